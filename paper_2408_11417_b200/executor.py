@@ -1,0 +1,389 @@
+"""GEMM entry point: run a Stream-K++ schedule on the B200.
+
+Drop-in for ``gemmsched.executor`` (reference ``executor.py``).  The
+reference executes each ``WorkItem`` on the host as
+``c[r0:r1,c0:c1] += a[r0:r1,k0:k1] @ b[k0:k1,c0:c1]`` in float64
+(executor.py:51-124).  Here :func:`execute_schedule` hands the whole schedule
+to one persistent sm_100a kernel through ``skpp_gemm_launch``: fp16/bf16
+operands, fp32 tensor-core accumulation, and a deterministic fixed-order
+partial-tile fixup instead of atomic adds.  There is no CPU fallback — on a
+machine without a B200 these functions raise.
+
+* ``execute_schedule(a, b, sched, tile, size, *, order, rng, workers)`` keeps
+  the reference signature and error messages.  numpy inputs are copied to
+  the GPU as ``in_dtype`` (default bf16) and the result comes back as float64
+  numpy; CUDA tensors stay on the device and return a CUDA tensor of
+  ``out_dtype`` (default fp32).  ``order``/``rng``/``workers`` are validated
+  as in the reference and otherwise have no effect: the device result does
+  not depend on completion order (the fixup order is fixed).
+* ``reference_gemm`` / ``random_int_matrix`` / ``run_equivalence`` mirror
+  executor.py:31-48, 127-145; ``reference_gemm`` is the reference's plain
+  float64 ``A @ B`` oracle used only for the equivalence report.
+* :func:`gemm` is the tensor-level API (policy instead of a materialised
+  schedule) used by the sweep and the benchmark.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .scheduler import Schedule, build_schedule, closed_form, grid_info
+from .types import HardwareModel, Policy, ProblemSize, TileShape
+
+try:
+    import torch
+except ImportError as exc:  # pragma: no cover - torch is part of the image
+    raise ImportError("paper_2408_11417_b200.executor needs torch for device memory") from exc
+
+DEFAULT_GEMM_TILE = TileShape(128, 128, 64)
+
+_IN_DTYPES = {torch.float16: _lib.F16, torch.bfloat16: _lib.BF16}
+_OUT_DTYPES = {torch.float32: _lib.F32, torch.float16: _lib.F16, torch.bfloat16: _lib.BF16}
+_NAMED = {
+    "fp16": torch.float16,
+    "float16": torch.float16,
+    "bf16": torch.bfloat16,
+    "bfloat16": torch.bfloat16,
+    "fp32": torch.float32,
+    "float32": torch.float32,
+}
+
+
+def _as_dtype(d, default):
+    if d is None:
+        return default
+    if isinstance(d, str):
+        return _NAMED[d.lower()]
+    return d
+
+
+@dataclass(frozen=True, slots=True)
+class EquivalenceReport:
+    exact_match: bool
+    max_abs_diff: float
+
+
+def reference_gemm(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """float64 ``A @ B`` oracle (executor.py:31-41)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.ndim != 2 or b.ndim != 2:
+        raise ValueError("reference_gemm expects 2-D matrices")
+    if a.shape[1] != b.shape[0]:
+        raise ValueError(f"inner dimensions disagree: A is {a.shape}, B is {b.shape}")
+    return a @ b
+
+
+def random_int_matrix(
+    rows: int, cols: int, rng: np.random.Generator, lo: int = -8, hi: int = 8
+) -> np.ndarray:
+    """Integer-valued float64 matrix, exact under any summation order (executor.py:44-48)."""
+    return rng.integers(lo, hi + 1, size=(rows, cols)).astype(np.float64)
+
+
+# -- device plumbing ----------------------------------------------------------
+
+_tls = threading.local()
+_ws_lock = threading.Lock()
+_workspaces: dict[tuple[int, int], torch.Tensor] = {}
+_sm_counts: dict[int, int] = {}
+
+
+def _require_cuda() -> int:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "the Stream-K++ GEMM runs only on a CUDA device (sm_100a B200); "
+            "there is no CPU fallback"
+        )
+    dev = torch.cuda.current_device()
+    if getattr(_tls, "device", None) != dev:
+        _lib.check(_lib.lib.skpp_set_device(dev))
+        _tls.device = dev
+    return dev
+
+
+def sm_count(device: int | None = None) -> int:
+    """Streaming multiprocessors of the device (148 on a B200)."""
+    dev = _require_cuda() if device is None else device
+    if dev not in _sm_counts:
+        n = ctypes.c_int32()
+        _lib.check(_lib.lib.skpp_device_info(dev, ctypes.byref(n), None, None))
+        _sm_counts[dev] = int(n.value)
+    return _sm_counts[dev]
+
+
+def max_coresident(tile: TileShape) -> int:
+    _require_cuda()
+    n = ctypes.c_int32()
+    _lib.check(
+        _lib.lib.skpp_max_coresident(_lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k), ctypes.byref(n))
+    )
+    return int(n.value)
+
+
+def tile_supported(tile: TileShape) -> bool:
+    return bool(_lib.lib.skpp_tile_supported(_lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k)))
+
+
+def workspace_for(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
+    """Zero-initialised fixup workspace, cached per (device, stream).
+
+    The kernel returns every flag to zero when it completes, so a cached
+    buffer can be reused by the next launch on the same stream.
+    """
+    key = (device, stream_handle)
+    with _ws_lock:
+        buf = _workspaces.get(key)
+        if buf is None or buf.numel() < nbytes:
+            size = max(nbytes, 1 << 20)
+            buf = torch.zeros(size, dtype=torch.uint8, device=f"cuda:{device}")
+            _workspaces[key] = buf
+        return buf
+
+
+class GemmPlan:
+    """A prepared launch: C = A @ B under one policy, reusable and graph-capturable.
+
+    All ctypes structures are built once; :meth:`launch` is a single call into
+    ``skpp_gemm_launch`` on the current stream.
+    """
+
+    def __init__(
+        self,
+        a: torch.Tensor,
+        b: torch.Tensor,
+        c: torch.Tensor,
+        policy: Policy,
+        tile: TileShape = DEFAULT_GEMM_TILE,
+        g: int | None = None,
+        trace_cap: int = 0,
+    ):
+        dev = _require_cuda()
+        if a.dim() != 2 or b.dim() != 2 or c.dim() != 2:
+            raise ValueError("gemm expects 2-D matrices")
+        if a.shape[1] != b.shape[0]:
+            raise ValueError(f"inner dimensions disagree: A is {tuple(a.shape)}, B is {tuple(b.shape)}")
+        if tuple(c.shape) != (a.shape[0], b.shape[1]):
+            raise ValueError("output shape does not match (m, n)")
+        if a.dtype not in _IN_DTYPES or b.dtype != a.dtype:
+            raise ValueError("A and B must both be float16 or both bfloat16")
+        if c.dtype not in _OUT_DTYPES:
+            raise ValueError("output must be float32, float16 or bfloat16")
+        for name, t in (("A", a), ("B", b), ("C", c)):
+            if not t.is_cuda:
+                raise ValueError(f"{name} must be a CUDA tensor")
+            if t.stride(1) != 1:
+                raise ValueError(f"{name} must be row-major (unit column stride)")
+        if not tile_supported(tile):
+            raise ValueError(
+                f"tile {tile.blk_m}x{tile.blk_n}x{tile.blk_k} is not implemented by the sm_100a "
+                "kernel (blk_m=128, blk_n in {64,128,256}, blk_k in {16,32,64})"
+            )
+        m, k = a.shape
+        n = b.shape[1]
+        self.size = ProblemSize(int(m), int(n), int(k))
+        self.tile = tile
+        self.policy = policy
+        self.g = sm_count(dev) if g is None else int(g)
+        self.a, self.b, self.c = a, b, c
+        self.device = dev
+        self._problem = _lib.Problem(m, n, k)
+        self._tile = _lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k)
+        self.sched_c = closed_form(self.size, tile, self.g, policy)
+        from .scheduler import policy_to_c
+
+        self._policy = policy_to_c(policy)
+        self._ops = _lib.Operands(
+            a.data_ptr(),
+            a.stride(0),
+            b.data_ptr(),
+            b.stride(0),
+            c.data_ptr(),
+            c.stride(0),
+            _IN_DTYPES[a.dtype],
+            _OUT_DTYPES[c.dtype],
+        )
+        self.ws_bytes = int(_lib.lib.skpp_workspace_bytes(self._problem, self._tile, self.g))
+        self.trace_cap = int(trace_cap)
+        if self.trace_cap:
+            self.trace = torch.full(
+                (self.g, self.trace_cap, _lib.TRACE_FIELDS), -1, dtype=torch.int64, device=a.device
+            )
+            self.trace_counts = torch.zeros(self.g, dtype=torch.int64, device=a.device)
+        else:
+            self.trace = self.trace_counts = None
+
+    @property
+    def uses_fixup(self) -> bool:
+        return self.sched_c.sk_tiles > 0
+
+    def launch(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        handle = st.cuda_stream
+        ws = workspace_for(self.ws_bytes, self.device, handle) if self.uses_fixup else None
+        rc = _lib.lib.skpp_gemm_launch(
+            self._problem,
+            self._tile,
+            self._policy,
+            self.g,
+            self._ops,
+            ws.data_ptr() if ws is not None else None,
+            self.ws_bytes if ws is not None else 0,
+            self.trace.data_ptr() if self.trace is not None else None,
+            self.trace_cap,
+            self.trace_counts.data_ptr() if self.trace_counts is not None else None,
+            handle,
+        )
+        if rc != _lib.OK:
+            msg = _lib.last_error()
+            if rc in (_lib.ETILE, _lib.EALIGN, _lib.EINVAL, _lib.EGRID, _lib.EWORKSPACE):
+                raise ValueError(msg)
+            raise _lib.SkppError(rc, msg)
+        return self.c
+
+    def trace_items(self) -> list[list[tuple[int, int, int, int, int, int]]]:
+        """Per-CTA items recorded by the last traced launch (device -> host)."""
+        if self.trace is None:
+            raise ValueError("plan was built without trace_cap")
+        counts = self.trace_counts.cpu().tolist()
+        rows = self.trace.cpu().numpy()
+        out = []
+        for x in range(self.g):
+            cnt = int(counts[x])
+            if cnt > self.trace_cap:
+                raise ValueError(f"CTA {x} recorded {cnt} items > trace_cap {self.trace_cap}")
+            out.append([tuple(int(v) for v in r) for r in rows[x, :cnt]])
+        return out
+
+
+def gemm(
+    a: torch.Tensor,
+    b: torch.Tensor,
+    policy: Policy,
+    *,
+    tile: TileShape = DEFAULT_GEMM_TILE,
+    g: int | None = None,
+    out: torch.Tensor | None = None,
+    out_dtype: torch.dtype = torch.float32,
+) -> torch.Tensor:
+    """C = A @ B on the current CUDA stream under a Stream-K++ policy."""
+    if out is None:
+        out = torch.empty((a.shape[0], b.shape[1]), dtype=out_dtype, device=a.device)
+    return GemmPlan(a, b, out, policy, tile, g).launch()
+
+
+def _pad_cols(t: torch.Tensor, mult: int = 8) -> torch.Tensor:
+    """Zero-pad the column count to a multiple of `mult` (TMA needs 16-byte row strides)."""
+    cols = t.shape[1]
+    if cols % mult == 0 and t.stride(1) == 1 and t.stride(0) % mult == 0:
+        return t
+    padded = torch.zeros((t.shape[0], (cols + mult - 1) // mult * mult), dtype=t.dtype, device=t.device)
+    padded[:, :cols] = t
+    return padded
+
+
+def _check_closed_form(sched: Schedule, size: ProblemSize, tile: TileShape) -> None:
+    mark = getattr(sched, "_skpp_closed_form", None)
+    if mark is not None and mark[0] == size and mark[1] == tile and mark[2] is sched.assignments:
+        return
+    expected = build_schedule(size, tile, HardwareModel(sched.g, 1), sched.policy)
+    if expected.assignments != sched.assignments:
+        raise ValueError(
+            "schedule differs from the closed form of its policy; the device kernel "
+            "executes policy schedules (build_schedule output) only"
+        )
+
+
+def execute_schedule(
+    a,
+    b,
+    sched: Schedule,
+    tile: TileShape,
+    size: ProblemSize,
+    *,
+    order: str = "scheduled",
+    rng: np.random.Generator | None = None,
+    workers: int = 1,
+    in_dtype=None,
+    out_dtype=None,
+):
+    """Run every work item of ``sched`` on the GPU and return C = A @ B."""
+    is_torch = isinstance(a, torch.Tensor)
+    if is_torch:
+        a_shape, b_shape = tuple(a.shape), tuple(b.shape)
+    else:
+        a = np.asarray(a, dtype=np.float64)
+        b = np.asarray(b, dtype=np.float64)
+        a_shape, b_shape = a.shape, b.shape
+    if a_shape != (size.m, size.k) or b_shape != (size.k, size.n):
+        raise ValueError(
+            f"matrix shapes {a_shape} x {b_shape} do not match "
+            f"problem size ({size.m}, {size.n}, {size.k})"
+        )
+    if sched.grid != grid_info(size, tile):
+        raise ValueError("schedule was built for a different problem/tile")
+    if order == "shuffled":
+        if rng is None:
+            raise ValueError('order="shuffled" requires an rng')
+    elif order != "scheduled":
+        raise ValueError(f"unknown order {order!r}")
+    _check_closed_form(sched, size, tile)
+
+    dev = _require_cuda()
+    if is_torch:
+        if not a.is_cuda:
+            a = a.cuda()
+            b = b.cuda()
+        op_dtype = a.dtype if a.dtype in _IN_DTYPES else _as_dtype(in_dtype, torch.bfloat16)
+        res_dtype = _as_dtype(out_dtype, torch.float32)
+        ad = a.to(op_dtype)
+        bd = b.to(op_dtype)
+    else:
+        op_dtype = _as_dtype(in_dtype, torch.bfloat16)
+        res_dtype = _as_dtype(out_dtype, torch.float32)
+        ad = torch.from_numpy(a).to(op_dtype).pin_memory().to(f"cuda:{dev}", non_blocking=True)
+        bd = torch.from_numpy(b).to(op_dtype).pin_memory().to(f"cuda:{dev}", non_blocking=True)
+    ad = _pad_cols(ad)
+    bd = _pad_cols(bd)
+    if ad.shape[1] != size.k:
+        # K was padded for A's row stride: pad B's rows to the same K with zeros.
+        bk = torch.zeros((ad.shape[1], bd.shape[1]), dtype=bd.dtype, device=bd.device)
+        bk[: size.k] = bd
+        bd = bk
+    c = torch.empty((size.m, bd.shape[1]), dtype=res_dtype, device=ad.device)
+    # Padding K or N up to a multiple of 8 never changes ceil(K/blk_k) or
+    # ceil(N/blk_n) (the implemented blk_n/blk_k are multiples of 8), so the
+    # launched schedule is the caller's; padded K only adds zero products.
+    GemmPlan(ad, bd, c, sched.policy, tile, sched.g).launch()
+    out = c[:, : size.n]
+    if is_torch:
+        return out
+    return out.to(torch.float64).cpu().numpy()
+
+
+def run_equivalence(
+    size: ProblemSize,
+    tile: TileShape,
+    hw: HardwareModel,
+    policy: Policy,
+    rng_seed: int,
+    *,
+    in_dtype="bf16",
+) -> EquivalenceReport:
+    """Build, execute on the GPU and compare one instance (executor.py:127-145)."""
+    rng = np.random.default_rng(rng_seed)
+    a = random_int_matrix(size.m, size.k, rng)
+    b = random_int_matrix(size.k, size.n, rng)
+    sched = build_schedule(size, tile, hw, policy)
+    got = execute_schedule(a, b, sched, tile, size, in_dtype=in_dtype)
+    want = reference_gemm(a, b)
+    diff = np.abs(got - want)
+    return EquivalenceReport(
+        exact_match=bool(np.array_equal(got, want)),
+        max_abs_diff=float(diff.max()) if diff.size else 0.0,
+    )

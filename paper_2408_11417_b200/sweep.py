@@ -1,0 +1,209 @@
+"""GPU autotuning sweep: measure every (size, policy) schedule on the B200.
+
+Replaces the analytic ``tune_grid`` loop of the reference
+(pipeline.py:102-114 -> costmodel.py:141-164 ``pick_winner``): each
+(size, policy) is timed on the device instead of costed by a formula.
+
+* Policies whose closed forms coincide (same data-parallel/Stream-K split and
+  order — e.g. every hybrid equals all-Stream-K when the grid has fewer tiles
+  than SMs) execute identical work; each distinct schedule is measured once
+  and its time is credited to all policies that share it, so the ranking's
+  ordinal tie-break picks the lowest one (costmodel.py:158).
+* One measurement = ``warmup`` launches, then ``reps`` CUDA-graph replays of
+  ``inner`` back-to-back launches timed with CUDA events on the launching
+  stream; the cost is the median per-launch time (paper protocol: warm-up +
+  mean of repeated launches).
+* Operands live in preallocated device buffers sized for the largest problem
+  of the sweep; problem views are carved from them, so the sweep allocates
+  nothing per size.
+* Multi-GPU: :func:`lpt_partition` splits the sizes over ranks by estimated
+  cost (longest processing time first); ranks share nothing on the data path
+  and their records are merged on the host — bank bytes do not depend on the
+  partition because ``build_bank`` inserts in lexicographic order.
+"""
+
+from __future__ import annotations
+
+import heapq
+import math
+import time
+from dataclasses import dataclass
+
+import torch
+
+from .costmodel import CostEstimate, TuneRecord, rank_costs
+from .executor import GemmPlan, sm_count
+from .scheduler import count_partials, schedule_signature
+from .types import Policy, ProblemSize, TileShape, canonical_policies
+
+DENSE_BF16_PEAK_TFLOPS = 2250.0  # nominal dense bf16/fp16 (148 SM x 8192 FLOP/clk x ~1.86 GHz)
+
+
+@dataclass(frozen=True)
+class MeasureParams:
+    warmup: int = 3
+    reps: int = 10
+    target_us: float = 200.0   # aim for graph replays of roughly this length
+    max_inner: int = 64
+    in_dtype: torch.dtype = torch.bfloat16
+    out_dtype: torch.dtype = torch.float32
+    peak_tflops: float = DENSE_BF16_PEAK_TFLOPS
+    use_graphs: bool = True
+
+
+class OperandPool:
+    """Device buffers large enough for every problem of a sweep."""
+
+    def __init__(self, sizes: list[ProblemSize], in_dtype=torch.bfloat16, out_dtype=torch.float32,
+                 device: int | None = None, seed: int = 0):
+        dev = torch.cuda.current_device() if device is None else device
+        max_a = max(s.m * _pad8(s.k) for s in sizes)
+        max_b = max(_pad8(s.k) * _pad8(s.n) for s in sizes)
+        max_c = max(s.m * _pad8(s.n) for s in sizes)
+        gen = torch.Generator(device=f"cuda:{dev}")
+        gen.manual_seed(seed)
+        self.a = torch.randn(max_a, generator=gen, device=f"cuda:{dev}", dtype=torch.float32).to(in_dtype)
+        self.b = torch.randn(max_b, generator=gen, device=f"cuda:{dev}", dtype=torch.float32).to(in_dtype)
+        self.c = torch.empty(max_c, device=f"cuda:{dev}", dtype=out_dtype)
+
+    def views(self, size: ProblemSize):
+        kp, np_ = _pad8(size.k), _pad8(size.n)
+        a = self.a[: size.m * kp].view(size.m, kp)[:, : size.k]
+        b = self.b[: kp * np_].view(kp, np_)[: size.k, : size.n]
+        c = self.c[: size.m * np_].view(size.m, np_)[:, : size.n]
+        return a, b, c
+
+
+def _pad8(v: int) -> int:
+    return (v + 7) // 8 * 8
+
+
+def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None) -> float:
+    """Median per-launch device time (microseconds) of a prepared GEMM."""
+    stream = torch.cuda.current_stream()
+    for _ in range(params.warmup):
+        plan.launch()
+    torch.cuda.synchronize()
+    if est_us is None:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        plan.launch()
+        t1.record(stream)
+        t1.synchronize()
+        est_us = max(t0.elapsed_time(t1) * 1e3, 1.0)
+    inner = int(max(1, min(params.max_inner, params.target_us // est_us)))
+    if params.use_graphs:
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                for _ in range(inner):
+                    plan.launch()
+        stream.wait_stream(side)
+        run = graph.replay
+        graph.replay()
+    else:
+        def run():
+            for _ in range(inner):
+                plan.launch()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(params.reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e3 / inner)
+    times.sort()
+    return times[len(times) // 2]
+
+
+def measure_size(
+    size: ProblemSize,
+    tile: TileShape,
+    g: int,
+    policies: list[Policy],
+    params: MeasureParams,
+    pool: OperandPool,
+) -> TuneRecord:
+    """Time every policy's schedule for one size (identical schedules measured once)."""
+    a, b, c = pool.views(size)
+    by_sig: dict[tuple, CostEstimate] = {}
+    costs = []
+    for pol in policies:
+        plan = GemmPlan(a, b, c, pol, tile, g)
+        sig = schedule_signature(plan.sched_c)
+        est = by_sig.get(sig)
+        if est is None:
+            us = time_plan(plan, params)
+            tflops = size.flops / (us * 1e-6) / 1e12
+            partial, full, _ = count_partials(plan.sched_c)
+            est = CostEstimate(makespan=us, utilization=tflops / params.peak_tflops,
+                               atomic_writes=partial, full_stores=full)
+            by_sig[sig] = est
+        costs.append((pol, est))
+    return rank_costs(size, costs)
+
+
+def tune_sizes(
+    sizes: list[ProblemSize],
+    tile: TileShape,
+    g: int | None = None,
+    policies: list[Policy] | None = None,
+    params: MeasureParams | None = None,
+    pool: OperandPool | None = None,
+    progress=None,
+) -> list[TuneRecord]:
+    """Measured records for ``sizes`` on the current device, in input order."""
+    if policies is None:
+        policies = canonical_policies()
+    if params is None:
+        params = MeasureParams()
+    if g is None:
+        g = sm_count()
+    if pool is None:
+        pool = OperandPool(sizes, params.in_dtype, params.out_dtype)
+    out = []
+    for i, size in enumerate(sizes):
+        out.append(measure_size(size, tile, g, policies, params, pool))
+        if progress is not None:
+            progress(i + 1, len(sizes))
+    return out
+
+
+def estimated_cost_s(size: ProblemSize, n_policies: int = 7, peak_tflops: float = 1200.0,
+                     launch_us: float = 8.0, reps: int = 13) -> float:
+    """Rough wall time of measuring one size (for LPT partitioning)."""
+    per = size.flops / (peak_tflops * 1e12) + launch_us * 1e-6
+    return n_policies * reps * per
+
+
+def lpt_partition(sizes: list[ProblemSize], world: int, cost=estimated_cost_s) -> list[list[ProblemSize]]:
+    """Longest-processing-time-first assignment of sizes to `world` ranks."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    heap = [(0.0, r) for r in range(world)]
+    parts: list[list[ProblemSize]] = [[] for _ in range(world)]
+    for size in sorted(sizes, key=lambda s: (-cost(s), s.m, s.n, s.k)):
+        load, r = heapq.heappop(heap)
+        parts[r].append(size)
+        heapq.heappush(heap, (load + cost(size), r))
+    return parts
+
+
+def sweep_throughput(n_sizes: int, n_policies: int, seconds: float) -> float:
+    """(size, policy) evaluations per second."""
+    return n_sizes * n_policies / seconds if seconds > 0 else math.inf
+
+
+class Stopwatch:
+    def __enter__(self):
+        self.t0 = time.perf_counter()
+        return self
+
+    def __exit__(self, *exc):
+        self.seconds = time.perf_counter() - self.t0

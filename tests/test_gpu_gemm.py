@@ -1,0 +1,131 @@
+"""GPU parity of the sm_100a Stream-K++ GEMM (run on a B200 via gpurun).
+
+Integer inputs in [-8, 8] (executor.py:44-48 ``random_int_matrix``) are exact
+in fp16/bf16 and every partial sum is an integer below 2^24, so the fp32
+device result must equal the float64 oracle bit for bit under every policy
+and every fixup order.  Random-normal inputs are checked against a float64
+product of the same rounded operands with the tolerance stated per test.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import gemm as ogemm
+from oracle import schedule as osched
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _sk():
+    import paper_2408_11417_b200 as sk
+
+    return sk
+
+
+def _int_case(m, n, k, seed):
+    rng = np.random.default_rng(seed)
+    a = ogemm.random_int_matrix(m, k, rng)
+    b = ogemm.random_int_matrix(k, n, rng)
+    return a, b
+
+
+def _run(a, b, policy, tile, g=None, in_dtype=torch.bfloat16, out_dtype=torch.float32, trace_cap=0):
+    sk = _sk()
+    at = torch.from_numpy(a).to(in_dtype).cuda()
+    bt = torch.from_numpy(b).to(in_dtype).cuda()
+    c = torch.full((a.shape[0], b.shape[1]), float("nan"), dtype=out_dtype, device="cuda")
+    plan = sk.GemmPlan(at, bt, c, policy, tile, g, trace_cap=trace_cap)
+    plan.launch()
+    torch.cuda.synchronize()
+    return c, plan
+
+
+POLICIES = None
+
+
+def _policies():
+    sk = _sk()
+    return sk.canonical_policies() + [sk.Policy.hybrid(2, sk_first=False), sk.Policy.hybrid(7)]
+
+
+@pytest.mark.parametrize(
+    "m,n,k,blk_n,blk_k",
+    [
+        (128, 128, 64, 128, 64),      # one tile, one k-block
+        (256, 256, 256, 128, 64),
+        (1024, 1024, 1024, 128, 64),  # BASELINE cfg 1
+        (512, 512, 4096, 128, 64),    # cfg 2 shape at reduced K
+        (384, 640, 1088, 256, 64),
+        (200, 136, 520, 64, 32),      # ragged M/N/K, BK=32
+        (130, 72, 48, 64, 16),        # ragged, BK=16
+    ],
+)
+def test_integer_inputs_bitwise_every_policy(m, n, k, blk_n, blk_k):
+    sk = _sk()
+    a, b = _int_case(m, n, k, seed=m + n + k)
+    want = ogemm.reference_gemm(a, b)
+    tile = sk.TileShape(128, blk_n, blk_k)
+    for pol in _policies():
+        got, _ = _run(a, b, pol, tile)
+        g = got.double().cpu().numpy()
+        assert np.array_equal(g, want), (pol.label, float(np.nanmax(np.abs(g - want))))
+
+
+@pytest.mark.parametrize("g", [1, 5, 37, 148])
+def test_grid_sizes(g):
+    sk = _sk()
+    a, b = _int_case(256, 384, 640, seed=g)
+    want = ogemm.reference_gemm(a, b)
+    for pol in (sk.Policy.data_parallel(), sk.Policy.hybrid(1), sk.Policy.all_stream_k()):
+        got, _ = _run(a, b, pol, sk.TileShape(128, 128, 64), g=g)
+        assert np.array_equal(got.double().cpu().numpy(), want), (g, pol.label)
+
+
+def test_device_trace_matches_closed_form_and_oracle():
+    sk = _sk()
+    size = sk.ProblemSize(1024, 1024, 1024)
+    tile = sk.TileShape(128, 128, 64)
+    a, b = _int_case(1024, 1024, 1024, seed=1)
+    for pol in _policies():
+        _, plan = _run(a, b, pol, tile, trace_cap=64)
+        dev = plan.trace_items()
+        want = osched.build_schedule(size.m, size.n, size.k, 128, 128, 64, 148, pol.kind.value, pol.sk_batches, pol.sk_first)
+        got = [[(t, kb, ke, wm, ph) for (t, kb, ke, wm, ph, _role) in wg] for wg in dev]
+        assert got == want, pol.label
+
+
+def test_fp16_and_output_dtypes():
+    sk = _sk()
+    a, b = _int_case(512, 256, 1024, seed=7)
+    want = ogemm.reference_gemm(a, b)
+    for in_dt in (torch.float16, torch.bfloat16):
+        for out_dt in (torch.float32, torch.bfloat16, torch.float16):
+            got, _ = _run(a, b, sk.Policy.all_stream_k(), sk.TileShape(128, 128, 64), in_dtype=in_dt, out_dtype=out_dt)
+            ref = torch.from_numpy(want).to(out_dt).double().numpy()
+            assert np.array_equal(got.double().cpu().numpy(), ref), (in_dt, out_dt)
+
+
+def test_randn_within_tolerance_and_deterministic():
+    sk = _sk()
+    m, n, k = 512, 512, 16384  # BASELINE cfg 2
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(0)
+    a = torch.randn(m, k, generator=gen, device="cuda").to(torch.bfloat16)
+    b = torch.randn(k, n, generator=gen, device="cuda").to(torch.bfloat16)
+    ref = (a.double() @ b.double())
+    tol = 1e-5 * ref.abs().max().item() * (k / 1024) ** 0.5
+    outs = []
+    for pol in sk.canonical_policies():
+        c = sk.gemm(a, b, pol)
+        torch.cuda.synchronize()
+        err = (c.double() - ref).abs().max().item()
+        assert err <= tol, (pol.label, err, tol)
+        if pol == sk.Policy.all_stream_k():
+            outs.append(c)
+    base = outs[0]
+    for _ in range(10):
+        again = sk.gemm(a, b, sk.Policy.all_stream_k())
+        torch.cuda.synchronize()
+        assert torch.equal(again, base)
