@@ -8,6 +8,7 @@ with the repository snapshot to the GPU box.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -39,11 +40,27 @@ def _nvcc() -> str:
     return cand
 
 
+HASH_PATH = LIB_PATH.with_name(LIB_PATH.name + ".srchash")
+
+
+def source_hash() -> str:
+    """Content hash of every source and header plus the compile flags."""
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for p in SOURCES + HEADERS:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
 def is_stale() -> bool:
-    if not LIB_PATH.exists():
+    """True when the library is missing or was built from different sources.
+
+    Content hashes (not mtimes) so that a copied checkout, e.g. the snapshot
+    shipped to a GPU box, does not trigger a rebuild.
+    """
+    if not LIB_PATH.exists() or not HASH_PATH.exists():
         return True
-    built = LIB_PATH.stat().st_mtime
-    return any(p.stat().st_mtime > built for p in SOURCES + HEADERS)
+    return HASH_PATH.read_text().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -59,6 +76,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         tmp.unlink(missing_ok=True)
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB_PATH)
+    HASH_PATH.write_text(source_hash() + "\n")
     return LIB_PATH
 
 
