@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Stream-K++ on B200 — headline benchmark (one JSON line on rank 0).
+
+Metric (BASELINE.json): "GEMM TFLOP/s vs dense TC peak; % shapes within 20%
+of oracle policy".  Default workload = BASELINE config 2: the skinny,
+split-K-bound bf16 GEMM M=N=512, K=16384 with fp32 output, under the policy
+the Stream-K++ selection layer picks:
+
+  1. selection (untimed): every canonical policy's schedule is measured on
+     the device (identical schedules once), a Bloom bank is built from the
+     winner, and the selected policy is the fastest measured candidate of
+     ``bank.query(size) | {data-parallel}``;
+  2. timed region: K steps, one persistent-kernel launch per step, L2
+     flushed (256 MiB write) before every step outside the per-step CUDA
+     events; device time is the sum of per-step event times, max over ranks.
+
+Also reported: ``e2e`` (the same GEMM through the public
+``execute_schedule`` with pinned host bf16 inputs, H2D + kernel + D2H every
+step, wall clock), ``roofline`` for the GEMM kernel, ``cpu_baseline`` (the
+oracle's float64 numpy port of the reference executor on this box's cores)
+and per-policy TFLOP/s from the selection sweep.
+
+``--impl reference`` times the reference's CPU implementation of the path
+(the oracle port of gemmsched's execute_schedule, float64 numpy/OpenBLAS,
+all host cores) on the same workload; under torchrun only rank 0 runs it.
+With N GPUs each rank runs the same GEMM (the GEMM runs on one GPU;
+replicas only), so ``value`` is N x the per-replica throughput ("weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GEMM TFLOP/s vs dense TC peak; % shapes within 20% of oracle policy"
+
+WORKLOADS = {
+    "cfg2": dict(m=512, n=512, k=16384, dtype="bf16", tile=(128, 128, 64),
+                 desc="BASELINE cfg2: skinny split-K-bound bf16 GEMM M=N=512 K=16384, fp32 out, "
+                      "Bloom-selected policy among the 7 canonical policies"),
+    "cfg1": dict(m=1024, n=1024, k=1024, dtype="fp16", tile=(128, 128, 64),
+                 desc="BASELINE cfg1: fp16 GEMM 1024^3, fp32 out, Bloom-selected policy (DP vs hybrid1)"),
+    "square8192": dict(m=8192, n=8192, k=8192, dtype="bf16", tile=(128, 256, 64),
+                       desc="large square bf16 GEMM 8192^3, fp32 out (70%-of-peak target)"),
+}
+
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+REASON_FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+def load_peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return dict(FALLBACK_PEAKS)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    def __init__(self, gpu_index: int, period_ms: int = 50):
+        self.cmd = [
+            "nvidia-smi", f"--id={gpu_index}",
+            "--query-gpu=clocks.sm,clocks.max.sm,power.draw," + ",".join(
+                f"clocks_event_reasons.{r}" for r in REASON_FIELDS),
+            "--format=csv,noheader,nounits", f"-lms={period_ms}",
+        ]
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(self.cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3 + len(REASON_FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(REASON_FIELDS, parts[3:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def physical_gpu(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].strip().isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and n_gpus != world:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    return world, rank, local
+
+
+def roofline(flops: float, nbytes: float, seconds: float, peaks: dict) -> dict:
+    t_tc = flops / (peaks["bf16_tflops"] * 1e12)
+    t_hbm = nbytes / (peaks["hbm_gbs"] * 1e9)
+    if t_tc >= t_hbm:
+        ach = flops / seconds / 1e12
+        return {"bound": "tensor", "achieved": round(ach, 2), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": round(ach / peaks["bf16_tflops"], 4), "traffic": None,
+                "peak_source": peaks["source"] + ", burst bf16"}
+    ach = nbytes / seconds / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
+            "peak_source": peaks["source"] + ", copy bandwidth"}
+
+
+def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool, max_seconds: float,
+                    max_reps: int, seed: int = 0):
+    """Time the oracle port of the reference executor (float64) on this host."""
+    import numpy as np
+
+    from oracle import gemm as ogemm
+    from oracle import schedule as osched
+
+    m, n, k = wl["m"], wl["n"], wl["k"]
+    bm, bn, bk = wl["tile"]
+    rng = np.random.default_rng(seed)
+    a = ogemm.random_int_matrix(m, k, rng)
+    b = ogemm.random_int_matrix(k, n, rng)
+    sched = osched.build_schedule(m, n, k, bm, bn, bk, 148, policy_kind, sk_batches, sk_first)
+    n_tiles = -(-n // bn)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_reps and (time.perf_counter() - t_start) < max_seconds:
+        t0 = time.perf_counter()
+        ogemm.execute_schedule(a, b, sched, m, n, k, bm, bn, bk, n_tiles)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args, wl: dict) -> None:
+    world, rank, _ = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    m, n, k = wl["m"], wl["n"], wl["k"]
+    flops = 2.0 * m * n * k
+    # The reference ranks policies with its cost model; for T < g every
+    # Stream-K policy ties and the ordinal tie-break credits hybrid1.
+    pol = ("hybrid", 1, True)
+    cpu_oracle_gemm(wl, *pol, max_seconds=60, max_reps=args.warmup)  # warm-up
+    times = cpu_oracle_gemm(wl, *pol, max_seconds=600, max_reps=args.steps)
+    total = sum(times)
+    value = flops * len(times) / total / 1e12
+    line = {
+        "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(total / len(times) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (integer-valued float64, seed 0)",
+        "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]), "g": 148,
+                   "policy": "hybrid1", "l2": "n/a (CPU)"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"{len(times)} full {m}x{n}x{k} schedule executions "
+                                   f"(oracle port of gemmsched executor.py:51-112, float64 numpy/OpenBLAS)"},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def select_policy(size, tile, g, pool):
+    """Measure all canonical policies, build the bank, pick the best candidate of query | {DP}."""
+    import paper_2408_11417_b200 as sk
+    from paper_2408_11417_b200 import sweep
+
+    params = sweep.MeasureParams(warmup=3, reps=15, in_dtype=pool.a.dtype)
+    rec = sweep.measure_size(size, tile, g, sk.canonical_policies(), params, pool)
+    bank = sk.build_bank([rec])
+    cand = set(bank.query(size)) | {sk.Policy.data_parallel()}
+    chosen, est = min(((p, e) for p, e in rec.costs if p in cand),
+                      key=lambda pe: (pe[1].makespan, pe[0].sort_key()))
+    return chosen, rec, bank
+
+
+def run_ours(args, wl: dict) -> None:
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import paper_2408_11417_b200 as sk
+    from paper_2408_11417_b200 import sweep
+
+    peaks = load_peaks()
+    m, n, k = wl["m"], wl["n"], wl["k"]
+    in_dtype = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float16
+    size = sk.ProblemSize(m, n, k)
+    tile = sk.TileShape(*wl["tile"])
+    g = sk.executor.sm_count()
+    pool = sweep.OperandPool([size], in_dtype, torch.float32, seed=rank)
+    policy, rec, bank = select_policy(size, tile, g, pool)
+    a, b, c = pool.views(size)
+    plan = sk.GemmPlan(a, b, c, policy, tile, g)
+    flops = 2.0 * m * n * k
+    nbytes = 2.0 * (m * k + k * n) + 4.0 * m * n
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        plan.launch()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(physical_gpu(local)) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            plan.launch()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    per_step_s = total_ms / args.steps / 1e3
+    value = world * flops * args.steps / (total_ms / 1e3) / 1e12
+
+    # end to end through the public API with pinned host inputs
+    e2e_steps = min(args.steps, args.e2e_steps)
+    a_h = a.cpu().pin_memory()
+    b_h = b.cpu().pin_memory()
+    sched = sk.build_schedule(size, tile, sk.HardwareModel(g, 1), policy)
+    for _ in range(3):
+        sk.execute_schedule(a_h, b_h, sched, tile, size)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        out = sk.execute_schedule(a_h, b_h, sched, tile, size)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * flops * e2e_steps / e2e_total / 1e12
+    assert out.shape == (m, n)
+
+    if rank == 0:
+        cores = len(os.sched_getaffinity(0))
+        cpu_times = cpu_oracle_gemm(wl, policy.kind.value, policy.sk_batches, policy.sk_first,
+                                    max_seconds=args.cpu_seconds, max_reps=20)
+        cpu_value = flops / statistics.median(cpu_times) / 1e12
+        per_policy = {p.label: round(size.flops / (e.makespan * 1e-6) / 1e12, 2) for p, e in rec.costs}
+        best_us = min(e.makespan for _, e in rec.costs)
+        chosen_us = dict((p, e) for p, e in rec.costs)[policy].makespan
+        line = {
+            "metric": METRIC,
+            "value": round(value, 3),
+            "unit": "TFLOP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(per_step_s * 1e3, 5),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": wl["dtype"],
+            "data": "synthetic (randn operands, seeded)",
+            "config": {
+                "workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]), "g": g,
+                "policy": policy.label, "out_dtype": "fp32",
+                "l2": "flushed before every step (256 MiB write outside the per-step events)",
+                "parallelism": f"replicas x{world} (GEMM is single-GPU)",
+            },
+            "pct_of_dense_peak": {
+                "measured_bf16": round(value / world / peaks["bf16_tflops"], 4),
+                "spec_2250": round(value / world / 2250.0, 4),
+            },
+            "selection": {
+                "selected": policy.label, "oracle_best": rec.winner.label,
+                "selected_vs_oracle": round(chosen_us / best_us, 4),
+                "within_20pct": chosen_us <= 1.2 * best_us,
+                "candidates": [p.label for p in bank.query(size)],
+                "per_policy_tflops": per_policy,
+                "note": "per-policy times from CUDA-graph replays with warm L2 (selection sweep)",
+            },
+            "roofline": roofline(flops, nbytes, per_step_s, peaks),
+            "cpu_baseline": {
+                "value": round(cpu_value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                "sample": f"{len(cpu_times)} full {m}x{n}x{k} runs of the oracle port of gemmsched "
+                          f"execute_schedule (float64 numpy/OpenBLAS, policy {policy.label})",
+            },
+            "e2e": {
+                "value": round(e2e_value, 3), "unit": "TFLOP/s",
+                "h2d_bytes_per_step": int(2 * (m * k + k * n)), "d2h_bytes_per_step": int(4 * m * n),
+                "api": "paper_2408_11417_b200.execute_schedule(pinned host bf16 tensors)",
+                "steps": e2e_steps,
+            },
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

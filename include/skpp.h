@@ -103,14 +103,25 @@ uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_tile_t* t, uin
 /* Tile shapes the sm_100a kernel implements: blk_m == 128, blk_n in {64,128,256}, blk_k in {16,32,64}. */
 int skpp_tile_supported(const skpp_tile_t* t);
 /* Persistent Stream-K++ GEMM C = A @ B on the current device, stream-ordered.
-   The workspace must be zero-filled the first time it is used; the kernel
-   leaves every flag zero again when it completes.  trace/trace_counts may be
+   The workspace must be zero-filled the first time it is used; afterwards the
+   kernel keeps it consistent itself (epoch-tagged flags), so one workspace
+   serves any number of stream-ordered launches, including CUDA-graph replays.  trace/trace_counts may be
    NULL; otherwise each CTA x writes up to trace_cap items at
    trace[(x*trace_cap + i)*SKPP_TRACE_FIELDS] and its item count at trace_counts[x]. */
 int skpp_gemm_launch(const skpp_problem_t* p, const skpp_tile_t* t, const skpp_policy_t* pol,
                      uint32_t g, const skpp_operands_t* ops, void* workspace,
                      uint64_t workspace_bytes, int64_t* trace, uint64_t trace_cap,
                      int64_t* trace_counts, void* stream);
+/* Prepared launches (the hot path for repeated GEMMs and CUDA-graph capture):
+   skpp_plan_create validates, builds the schedule scalars and TMA descriptors
+   once; skpp_plan_launch only binds the workspace and launches on `stream`.
+   skpp_gemm_launch == create + launch + destroy. */
+int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t, const skpp_policy_t* pol,
+                     uint32_t g, const skpp_operands_t* ops, int64_t* trace, uint64_t trace_cap,
+                     int64_t* trace_counts, void** plan_out);
+uint64_t skpp_plan_workspace_bytes(const void* plan);
+int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_bytes, void* stream);
+void skpp_plan_destroy(void* plan);
 /* Decode-only kernel: every CTA walks its items with the GEMM's device decoder
    and records them (no math).  Same trace layout as skpp_gemm_launch. */
 int skpp_schedule_trace_device(const skpp_problem_t* p, const skpp_tile_t* t,
@@ -119,6 +130,13 @@ int skpp_schedule_trace_device(const skpp_problem_t* p, const skpp_tile_t* t,
 /* Make `device` current for this library's CUDA runtime on the calling thread
    (the caller's framework may use a different runtime instance). */
 int skpp_set_device(int device);
+/* Debug hook: when non-NULL, following launches write 16 %globaltimer stamps per CTA
+   (setup done, first load, first stage landed, last MMA, items done, flags seen,
+   reductions done, ...) to device_buffer[cta*16 + event].  NULL disables. */
+void skpp_debug_timeline(uint64_t* device_buffer);
+/* Tuning knob for launches made after the call: the TMA producer also prefetches
+   into L2 the k-blocks up to `k_blocks` ahead of the one it loads (0 = off). */
+void skpp_set_l2_prefetch(uint32_t k_blocks);
 /* SM count, compute capability and the co-resident CTA limit of the GEMM kernel for blk_n. */
 int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 int skpp_max_coresident(const skpp_tile_t* t, int32_t* ctas);

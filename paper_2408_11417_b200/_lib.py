@@ -112,11 +112,21 @@ SIGNATURES = {
             C.c_void_p,
         ],
     ),
+    "skpp_plan_create": (
+        C.c_int,
+        [_P(Problem), _P(Tile), _P(PolicyC), C.c_uint32, _P(Operands), C.c_void_p, C.c_uint64,
+         C.c_void_p, _P(C.c_void_p)],
+    ),
+    "skpp_plan_workspace_bytes": (C.c_uint64, [C.c_void_p]),
+    "skpp_plan_launch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "skpp_plan_destroy": (None, [C.c_void_p]),
     "skpp_schedule_trace_device": (
         C.c_int,
         [_P(Problem), _P(Tile), _P(PolicyC), C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p],
     ),
     "skpp_set_device": (C.c_int, [C.c_int]),
+    "skpp_debug_timeline": (None, [C.c_void_p]),
+    "skpp_set_l2_prefetch": (None, [C.c_uint32]),
     "skpp_device_info": (C.c_int, [C.c_int, _P(C.c_int32), _P(C.c_int32), _P(C.c_int32)]),
     "skpp_max_coresident": (C.c_int, [_P(Tile), _P(C.c_int32)]),
     "skpp_murmur3_x64_128": (None, [C.c_char_p, C.c_uint64, C.c_uint32, _u64p]),

@@ -5,21 +5,27 @@
 // on the host in float64, with the `+=` standing for the atomic fixup of
 // Algorithm 1.  Here one launch runs a whole schedule:
 //
-//   grid    = g CTAs (one per SM, co-resident), CTA x == workgroup x;
-//   warp 0  = TMA producer: walks x's items (skpp_sched.h) and streams the
-//             A (K-major, swizzled) and B (N-major, SW128) k-blocks of each
-//             item's [kb, ke) range through an S-stage shared-memory ring;
-//   warp 1  = MMA issuer: one thread issues tcgen05.mma kind::f16
-//             (M=128, N=BN, K=16) into an fp32 TMEM accumulator, double
-//             buffered across items; accumulate is reset at each item's kb;
-//   warp 2  = TMEM allocator;
-//   warps 4-7 = epilogue: tcgen05.ld rows of the accumulator and, by role,
-//             FULL  -> convert and store C,
-//             PEER  -> write the fp32 partial to workspace slot x, release flag[x],
-//             OWNER -> acquire flags of peers x+1..peer_hi, add their partials
-//                      in increasing CTA order (fixed => deterministic), store C.
-// Flags are self-cleaning (the owner zeroes each flag it consumed), so the
-// kernel is CUDA-graph replay safe without an epoch parameter.
+//   grid      = g CTAs (one per SM, co-resident), CTA x == workgroup x;
+//   warp 0    = TMA producer: walks x's items (skpp_sched.h) and streams the
+//               A (K-major, swizzled) and B (N-major, SW128) k-blocks of each
+//               item's [kb, ke) range through an S-stage shared-memory ring;
+//   warp 1    = MMA issuer: one thread issues tcgen05.mma kind::f16
+//               (M=128, N=BN, K=16) into an fp32 TMEM accumulator, double
+//               buffered across items; accumulate is reset at each item's kb;
+//   warp 2    = TMEM allocator;
+//   warps 4-7 = epilogue, two phases:
+//     phase 1, per item in order: tcgen05.ld the accumulator rows; a FULL
+//       item is packed into swizzled shared-memory staging (two 4 KiB buffers
+//       per warp) and TMA-stored to C; a partial item is written with
+//       coalesced stores to this CTA's workspace slot, whose flag is then
+//       released.  No CTA waits on another in phase 1.
+//     phase 2, after all items: for every split tile it touched, the CTA
+//       reduces ITS share of the tile's columns over ALL contributors' slots,
+//       pulled into the (now idle) operand ring with bulk copies, summed in
+//       increasing CTA order (fixed order => deterministic) and stored to C.
+//   Every CTA produces all its partials before it waits, so the wait graph
+//   is acyclic; flags carry an epoch kept in the workspace header, so the
+//   kernel is CUDA-graph replay safe.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -42,7 +48,12 @@ void set_error(const std::string& msg);  // skpp_host.cpp
 constexpr int kBM = 128;
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
-constexpr uint32_t kSmemBudget = 196608;  // operand ring budget (192 KiB)
+constexpr uint32_t kRingBudget = 196608;   // operand ring (192 KiB)
+constexpr uint32_t kStageBuf = 4096;       // one epilogue staging buffer: 32 rows x 128 B
+constexpr uint32_t kStagingBytes = 4 * 2 * kStageBuf;
+// Workspace: [256 B header][2g flags, 256-B rounded][2g slots x BM x BN fp32]
+constexpr uint64_t kWsHeader = 256;
+inline uint64_t ws_flag_bytes(uint64_t g) { return (2 * g * 4 + 255) / 256 * 256; }
 
 #ifndef SKPP_WATCHDOG_CYCLES
 #define SKPP_WATCHDOG_CYCLES (1ull << 35)  // ~17 s at 1.9 GHz: trap instead of hanging
@@ -64,17 +75,14 @@ __device__ __forceinline__ void watchdog(long long start, int where) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
 }
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -86,7 +94,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int where) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
@@ -100,6 +107,43 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// 1-D bulk copy global -> shared, completing on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -117,7 +161,6 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -125,9 +168,8 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
       : "memory");
 }
 
-// 32 lanes x 32 consecutive fp32 columns: thread (lane) gets its row's 32 values.
-__device__ __forceinline__ void tmem_ld_32(uint32_t taddr, float* v) {
-  uint32_t r[32];
+// 32 lanes x 32 consecutive fp32 columns: each thread gets its row's 32 values.
+__device__ __forceinline__ void tmem_ld_32(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
@@ -139,14 +181,12 @@ __device__ __forceinline__ void tmem_ld_32(uint32_t taddr, float* v) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
         "=r"(r[31])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void epi_bar_sync() {
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-}
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -156,12 +196,16 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ float4 ld_cg_f4(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
 }
 
 // UMMA shared-memory matrix descriptor (sm_100 format, version 1).
@@ -171,6 +215,15 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
 }
 
+__device__ __forceinline__ uint32_t pack2(float a, float b, int out_dtype) {
+  if (out_dtype == SKPP_BF16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
 // ------------------------------------------------------------ kernel config --
 
 template <int BN, int BK>
@@ -178,15 +231,16 @@ struct Cfg {
   static constexpr uint32_t A_BYTES = kBM * BK * 2;
   static constexpr uint32_t B_BYTES = BK * BN * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t STAGES_RAW = kSmemBudget / STAGE_BYTES;
-  static constexpr uint32_t STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr uint32_t STAGES_RAW = kRingBudget / STAGE_BYTES;
+  static constexpr uint32_t STAGES = STAGES_RAW > 32 ? 32 : STAGES_RAW;
+  static constexpr uint32_t RING_BYTES = STAGES * STAGE_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN <= 32    ? 32
                                         : 2 * BN <= 64  ? 64
                                         : 2 * BN <= 128 ? 128
                                         : 2 * BN <= 256 ? 256
                                                         : 512;
-  static constexpr uint32_t BAR_BYTES = 256;
-  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 16 + 1023) / 1024 * 1024;
+  static constexpr uint32_t SMEM = RING_BYTES + kStagingBytes + BAR_BYTES + 1024;
   // A: K-major, one swizzle atom along K (BK*2 bytes = 32/64/128 B)
   static constexpr uint32_t A_LAYOUT = BK == 64 ? 2u : (BK == 32 ? 4u : 6u);
   static constexpr uint32_t A_SBO = 8 * BK * 2;  // 8 rows of one atom
@@ -197,6 +251,7 @@ struct Cfg {
   static_assert(BN % 64 == 0 && BN <= 256, "BN");
   static_assert(BK == 16 || BK == 32 || BK == 64, "BK");
   static_assert(STAGES >= 2, "stages");
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 struct GemmParams {
@@ -206,13 +261,39 @@ struct GemmParams {
   int32_t out_dtype;
   void* C;
   uint64_t ldc;
-  uint32_t c_vec_ok;
-  float* ws;
-  uint32_t* flags;
+  uint32_t c_vec_ok;   // C base and row stride 16-byte aligned
+  uint32_t c_tma;      // C tensor map valid: phase-1 FULL tiles use TMA stores
+  float* ws;           // 2g partial slots of BM x BN fp32, row-major
+  uint32_t* flags;     // 2g slot flags (== epoch when the slot holds this launch's partial)
+  uint32_t* hdr;       // [0] epoch of the last completed launch, [1] CTAs done in this launch
   int64_t* trace;
   uint64_t trace_cap;
   int64_t* trace_counts;
+  uint64_t* timeline;  // debug: TL_EVENTS %globaltimer stamps per CTA, or null
+  uint32_t l2_prefetch; // k-blocks ahead to prefetch into L2 (0 = off)
 };
+
+// Debug timeline (skpp_debug_timeline): per-CTA %globaltimer stamps.
+enum : int {
+  TL_START = 0,       // all warps past setup (barriers + TMEM)
+  TL_FIRST_TMA = 1,   // producer issued its first load
+  TL_FIRST_FULL = 2,  // MMA saw its first stage land
+  TL_MMA_DONE = 3,    // MMA issued its last commit
+  TL_PHASE1 = 4,      // epilogue finished all items (stores / partials)
+  TL_WAITED = 5,      // epilogue finished waiting for the first split tile's flags
+  TL_PHASE2 = 6,      // epilogue finished the reductions
+  TL_EPI_FIRST = 8,   // epilogue saw its first accumulator
+  TL_PART_ISSUED = 9, // first partial: all TMA stores issued
+  TL_PART_FLAG = 10,  // first partial: flag released
+  TL_EVENTS = 16
+};
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SKPP_STAMP(p, ev) \
+  do { if ((p).timeline) (p).timeline[(uint64_t)blockIdx.x * TL_EVENTS + (ev)] = gtimer(); } while (0)
 
 __device__ __forceinline__ void record_item(const GemmParams& p, uint32_t x, uint64_t idx,
                                             const Item& it) {
@@ -226,57 +307,42 @@ __device__ __forceinline__ void record_item(const GemmParams& p, uint32_t x, uin
   r[5] = (int64_t)it.role;
 }
 
-// Convert and store 32 consecutive columns of one output row.
-__device__ __forceinline__ void store_row_chunk(const GemmParams& p, uint64_t row, uint64_t col0,
-                                                const float* v) {
-  if (row >= p.M || col0 >= p.N) return;
-  const bool full = p.c_vec_ok && col0 + 32 <= p.N;
+// Direct (non-TMA) store of one packed 128-byte row segment; used only when C
+// is not 16-byte aligned.  `w` holds 32 fp32 or 64 16-bit values.
+__device__ __forceinline__ void store_row_direct(const GemmParams& p, uint64_t row, uint64_t col0,
+                                                 const uint32_t* w) {
+  if (row >= p.M) return;
   if (p.out_dtype == SKPP_F32) {
-    float* c = reinterpret_cast<float*>(p.C) + row * p.ldc + col0;
+    float* c = reinterpret_cast<float*>(p.C) + row * p.ldc;
+    for (int j = 0; j < 32 && col0 + j < p.N; ++j) c[col0 + j] = __uint_as_float(w[j]);
+  } else {
+    uint16_t* c = reinterpret_cast<uint16_t*>(p.C) + row * p.ldc;
+    for (int j = 0; j < 64 && col0 + j < p.N; ++j)
+      c[col0 + j] = (uint16_t)(w[j >> 1] >> (16 * (j & 1)));
+  }
+}
+
+// Convert and store 4 consecutive columns of one output row (phase-2 reduction).
+__device__ __forceinline__ void store_vec4(const GemmParams& p, uint64_t row, uint64_t col,
+                                           float4 a) {
+  if (row >= p.M || col >= p.N) return;
+  const bool full = p.c_vec_ok && col + 4 <= p.N;
+  if (p.out_dtype == SKPP_F32) {
+    float* c = reinterpret_cast<float*>(p.C) + row * p.ldc + col;
     if (full) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        reinterpret_cast<float4*>(c)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      *reinterpret_cast<float4*>(c) = a;
     } else {
-      for (int j = 0; j < 32 && col0 + j < p.N; ++j) c[j] = v[j];
-    }
-  } else if (p.out_dtype == SKPP_BF16) {
-    __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + row * p.ldc + col0;
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint4 w;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j + 0], v[8 * j + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
-        memcpy(&w.x, &h0, 4);
-        memcpy(&w.y, &h1, 4);
-        memcpy(&w.z, &h2, 4);
-        memcpy(&w.w, &h3, 4);
-        reinterpret_cast<uint4*>(c)[j] = w;
-      }
-    } else {
-      for (int j = 0; j < 32 && col0 + j < p.N; ++j) c[j] = __float2bfloat16_rn(v[j]);
+      const float v[4] = {a.x, a.y, a.z, a.w};
+      for (int j = 0; j < 4 && col + j < p.N; ++j) c[j] = v[j];
     }
   } else {
-    __half* c = reinterpret_cast<__half*>(p.C) + row * p.ldc + col0;
+    uint16_t* c = reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + col;
+    const uint32_t lo = pack2(a.x, a.y, p.out_dtype), hi = pack2(a.z, a.w, p.out_dtype);
     if (full) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint4 w;
-        __half2 h0 = __floats2half2_rn(v[8 * j + 0], v[8 * j + 1]);
-        __half2 h1 = __floats2half2_rn(v[8 * j + 2], v[8 * j + 3]);
-        __half2 h2 = __floats2half2_rn(v[8 * j + 4], v[8 * j + 5]);
-        __half2 h3 = __floats2half2_rn(v[8 * j + 6], v[8 * j + 7]);
-        memcpy(&w.x, &h0, 4);
-        memcpy(&w.y, &h1, 4);
-        memcpy(&w.z, &h2, 4);
-        memcpy(&w.w, &h3, 4);
-        reinterpret_cast<uint4*>(c)[j] = w;
-      }
+      *reinterpret_cast<uint2*>(c) = make_uint2(lo, hi);
     } else {
-      for (int j = 0; j < 32 && col0 + j < p.N; ++j) c[j] = __float2half_rn(v[j]);
+      const uint32_t w[2] = {lo, hi};
+      for (int j = 0; j < 4 && col + j < p.N; ++j) c[j] = (uint16_t)(w[j >> 1] >> (16 * (j & 1)));
     }
   }
 }
@@ -284,18 +350,21 @@ __device__ __forceinline__ void store_row_chunk(const GemmParams& p, uint64_t ro
 template <int BN, int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     streamk_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using C = Cfg<BN, BK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* stg = smem + C::RING_BYTES;  // epilogue staging, 1024-aligned
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + kStagingBytes);
   uint64_t* empty_bar = full_bar + C::STAGES;
   uint64_t* tfull_bar = empty_bar + C::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* red_bar = tempty_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_bar + 1);
 
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
@@ -313,8 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 4);
     }
+    mbar_init(red_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fence_async_shared();
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -327,11 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) SKPP_STAMP(p, TL_START);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (1 lane)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      bool first_load = true;
       Cursor cur;
       cursor_init(cur, s, x);
       Item it;
@@ -341,12 +413,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint64_t kk = it.kb; kk < it.ke; ++kk) {
           mbar_wait(&empty_bar[stage], phase ^ 1, 1);
           mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          if (first_load) {
+            SKPP_STAMP(p, TL_FIRST_TMA);
+            first_load = false;
+          }
           const int32_t k0 = (int32_t)(kk * BK);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
 #pragma unroll
           for (int j = 0; j < BN / 64; ++j)
             tma_load_2d(sB + stage * C::B_BYTES + j * (BK * 128), &tmB, n0 + 64 * j, k0,
                         &full_bar[stage]);
+          if (p.l2_prefetch) {
+            // warm L2 with the k-blocks beyond the ring: up to p.l2_prefetch of them
+            const uint64_t far = kk + C::STAGES + p.l2_prefetch - 1;
+            const uint64_t near = (kk == it.kb) ? kk + C::STAGES : far;
+            for (uint64_t kq = near; kq <= far && kq < it.ke; ++kq) {
+              const int32_t kq0 = (int32_t)(kq * BK);
+              tma_prefetch_2d(&tmA, kq0, m0);
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_prefetch_2d(&tmB, n0 + 64 * j, kq0);
+            }
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -369,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint64_t kk = it.kb; kk < it.ke; ++kk) {
           mbar_wait(&full_bar[stage], phase, 3);
           tc_fence_after();
+          if (local == 0 && kk == it.kb) SKPP_STAMP(p, TL_FIRST_FULL);
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
@@ -386,13 +474,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&tfull_bar[as]);
         ++local;
       }
+      SKPP_STAMP(p, TL_MMA_DONE);
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------ epilogue (4 warps)
-    const uint32_t ew = warp - kEpiWarp0;  // TMEM lane quarter of this warp
-    const uint32_t row = ew * 32 + lane;    // tile row owned by this thread
-    const bool leader = (row == 0);
-    uint32_t local = 0;
+    const uint32_t ew = warp - kEpiWarp0;    // TMEM lane quarter / staging owner
+    const uint32_t row = ew * 32 + lane;      // tile row held by this thread
+    const uint32_t et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+    const bool leader = (et == 0);
+    const bool out16 = p.out_dtype != SKPP_F32;
+    const uint32_t epoch = s.sk_tiles ? (ld_relaxed_gpu(p.hdr) + 1u) : 0u;
+    const uint32_t stg_base = smem_u32(stg) + ew * 2 * kStageBuf;
+    uint32_t sbuf = 0;  // staging buffer toggle of this warp
+    uint64_t split_tiles[2];
+    uint32_t n_split = 0, sk_seen = 0, local = 0;
     Cursor cur;
     cursor_init(cur, s, x);
     Item it;
@@ -401,69 +496,185 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader) record_item(p, x, local, it);
       mbar_wait(&tfull_bar[as], aph, 4);
       tc_fence_after();
+      if (leader && local == 0) SKPP_STAMP(p, TL_EPI_FIRST);
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + as * BN;
-      const uint64_t grow = (it.tile / s.n_tiles) * kBM + row;
-      const uint64_t gcol = (it.tile % s.n_tiles) * BN;
-      float v[32];
-      if (it.role == ROLE_PEER) {
-        float4* slot = reinterpret_cast<float4*>(p.ws + (uint64_t)x * kBM * BN);
+      const bool partial = it.role != ROLE_FULL;
+      const uint64_t slot = 2ull * x + (sk_seen == 0 ? 0 : 1);
+      const uint64_t tile_row0 = (it.tile / s.n_tiles) * kBM;
+      const uint64_t tile_col0 = (it.tile % s.n_tiles) * BN;
+      if (partial) {
+        // Partial slot layout: float4[BN/4][BM] ("column-group major"): a warp's
+        // store of one column group is 32 consecutive rows = 512 contiguous bytes,
+        // and a contributor's share of columns is one contiguous range.
+        float4* dst = reinterpret_cast<float4*>(p.ws + slot * (uint64_t)(kBM * BN)) + row;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
-          tmem_ld_32(taddr + c * 32, v);
+          uint32_t w[32];
+          tmem_ld_32(taddr + c * 32, w);
+          tmem_ld_wait();
+          if (c == BN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[as]);
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            slot[(c * 8 + j) * kBM + row] =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            dst[(c * 8 + j) * kBM] = make_float4(__uint_as_float(w[4 * j]), __uint_as_float(w[4 * j + 1]),
+                                                 __uint_as_float(w[4 * j + 2]), __uint_as_float(w[4 * j + 3]));
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[as]);
-        __threadfence();
+        if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_ISSUED);
+        // publish: every thread's stores happen-before the barrier; the leader's
+        // gpu-scope release then covers them (release is cumulative).
         epi_bar_sync();
-        if (leader) st_release_gpu(p.flags + x, 1u);
+        if (leader) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          st_release_gpu(p.flags + slot, epoch);
+        }
+        if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_FLAG);
+        split_tiles[n_split++] = it.tile - s.dp_tiles;
       } else {
-        if (it.role == ROLE_OWNER) {
-          if (leader) {
-            for (uint64_t q = x + 1; q <= it.peer_hi; ++q) {
-              if (ld_acquire_gpu(p.flags + q) != 1u) {
-                const long long t0 = clock64();
-                while (ld_acquire_gpu(p.flags + q) != 1u) {
-                  __nanosleep(64);
-                  watchdog(t0, 5);
-                }
-              }
-              p.flags[q] = 0u;  // consumed: self-cleaning for the next launch
-            }
-          }
-          epi_bar_sync();
-        }
+        // One chunk = 128 bytes of a row: 32 fp32 columns or 64 16-bit columns.
+        const int ccols = out16 ? 64 : 32;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          tmem_ld_32(taddr + c * 32, v);
-          if (it.role == ROLE_OWNER) {
-            for (uint64_t q = x + 1; q <= it.peer_hi; ++q) {
-              const float4* src = reinterpret_cast<const float4*>(p.ws + q * kBM * BN);
-              float4 t[8];
+        for (int c = 0; c < BN / ccols; ++c) {
+          uint32_t w[32];
+          if (out16) {
+            uint32_t r0[32], r1[32];
+            tmem_ld_32(taddr + c * 64, r0);
+            tmem_ld_32(taddr + c * 64 + 32, r1);
+            tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 8; ++j) t[j] = ld_cg_f4(src + (c * 8 + j) * kBM + row);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                v[4 * j] += t[j].x;
-                v[4 * j + 1] += t[j].y;
-                v[4 * j + 2] += t[j].z;
-                v[4 * j + 3] += t[j].w;
-              }
+            for (int j = 0; j < 16; ++j) {
+              w[j] = pack2(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]), p.out_dtype);
+              w[16 + j] = pack2(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]), p.out_dtype);
             }
+          } else {
+            tmem_ld_32(taddr + c * 32, w);
+            tmem_ld_wait();
           }
-          store_row_chunk(p, grow, gcol + c * 32, v);
+          if (c == BN / ccols - 1) {
+            // all TMEM reads of this item complete: hand the accumulator stage back
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[as]);
+          }
+          if (p.c_tma) {
+            const uint32_t buf = stg_base + sbuf * kStageBuf;
+            if (lane == 0) bulk_wait_read<1>();  // the store that used `buf` has read it
+            __syncwarp();
+            const uint32_t rbase = buf + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              st_shared_v4(rbase + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                           w[4 * j + 3]);
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, stg + (buf - smem_u32(stg)), (int32_t)(tile_col0 + c * ccols),
+                           (int32_t)(tile_row0 + ew * 32));
+              bulk_commit();
+            }
+            sbuf ^= 1;
+          } else {
+            store_row_direct(p, tile_row0 + row, tile_col0 + c * ccols, w);
+          }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[as]);
       }
+      if (it.phase == PHASE_SK) ++sk_seen;
       ++local;
     }
     if (leader && p.trace_counts != nullptr) p.trace_counts[x] = (int64_t)local;
+    if (leader) SKPP_STAMP(p, TL_PHASE1);
+
+    // ---- phase 2: cooperative fixed-order reduction of the split tiles.
+    // Contributor idx of a tile with nc contributors reduces column groups
+    // [idx*V/nc, (idx+1)*V/nc) over all nc slots, in increasing CTA order.
+    // The slices are pulled into the operand ring (idle now: every MMA of this
+    // CTA has completed) with bulk copies; each thread owns one tile row.
+    constexpr uint32_t V = BN / 4;       // float4 column groups per tile row
+    constexpr uint32_t GB = kBM * 16;    // bytes of one column group (all rows)
+    constexpr uint32_t NG = 8;           // column groups per pass (register accumulators)
+    uint32_t red_phase = 0;
+    const float4* ring = reinterpret_cast<const float4*>(smem);
+    for (uint32_t si = 0; si < n_split; ++si) {
+      const uint64_t u = split_tiles[si];
+      const uint64_t x0 = (u * s.ipt) / s.ipw;
+      const uint64_t x1 = ((u + 1) * s.ipt - 1) / s.ipw;
+      const uint32_t nc = (uint32_t)(x1 - x0 + 1);
+      const uint32_t idx = (uint32_t)(x - x0);
+      const uint32_t j0 = (uint32_t)(((uint64_t)idx * V) / nc);
+      const uint32_t j1 = (uint32_t)(((uint64_t)(idx + 1) * V) / nc);
+      if (j0 == j1) continue;
+      // contributor x0+t wrote its first Stream-K item (slot 2(x0+t)), except
+      // x0 when its range starts inside an earlier tile (tile u is its last item)
+      const uint64_t slot0 = 2 * x0 + ((x0 * s.ipw == u * s.ipt) ? 0 : 1);
+      for (uint32_t t = et; t < nc; t += 128) {
+        const uint64_t sl = t == 0 ? slot0 : 2 * (x0 + t);
+        if (ld_acquire_gpu(p.flags + sl) != epoch) {
+          const long long t0 = clock64();
+          while (ld_acquire_gpu(p.flags + sl) != epoch) {
+            __nanosleep(32);
+            watchdog(t0, 5);
+          }
+        }
+      }
+      epi_bar_sync();
+      if (leader && si == 0) SKPP_STAMP(p, TL_WAITED);
+      const uint64_t tile = s.dp_tiles + u;
+      const uint64_t grow = (tile / s.n_tiles) * kBM + et;
+      const uint64_t gcol0 = (tile % s.n_tiles) * BN;
+      for (uint32_t jb = j0; jb < j1; jb += NG) {
+        const uint32_t ng = (j1 - jb < NG) ? (j1 - jb) : NG;
+        const uint32_t bytes = ng * GB;
+        uint32_t tb = C::RING_BYTES / bytes;  // contributors per batch (>= 12)
+        if (tb > nc) tb = nc;
+        float4 acc[NG];
+#pragma unroll
+        for (uint32_t i = 0; i < NG; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t t0 = 0; t0 < nc; t0 += tb) {
+          const uint32_t nb = (nc - t0 < tb) ? (nc - t0) : tb;
+          if (leader) {
+            fence_async_global();
+            mbar_arrive_expect_tx(red_bar, nb * bytes);
+            for (uint32_t t = 0; t < nb; ++t) {
+              const uint64_t sl = (t0 + t) == 0 ? slot0 : 2 * (x0 + t0 + t);
+              bulk_g2s(smem + t * bytes, p.ws + sl * (uint64_t)(kBM * BN) + (uint64_t)jb * kBM * 4,
+                       bytes, red_bar);
+            }
+          }
+          mbar_wait(red_bar, red_phase, 6);
+          red_phase ^= 1;
+          for (uint32_t t = 0; t < nb; ++t) {
+#pragma unroll
+            for (uint32_t i = 0; i < NG; ++i) {
+              if (i < ng) {
+                const float4 q = ring[(t * ng + i) * kBM + et];
+                acc[i].x += q.x;
+                acc[i].y += q.y;
+                acc[i].z += q.z;
+                acc[i].w += q.w;
+              }
+            }
+          }
+          epi_bar_sync();  // the ring is overwritten by the next batch's copies
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < NG; ++i)
+          if (i < ng) store_vec4(p, grow, gcol0 + 4 * (jb + i), acc[i]);
+      }
+    }
+    if (leader) SKPP_STAMP(p, TL_PHASE2);
+    if (lane == 0) bulk_wait<0>();  // staging must outlive the in-flight TMA stores
+    // ---- launch epilogue: the last CTA out advances the workspace epoch
+    if (s.sk_tiles && leader) {
+      __threadfence();
+      const uint32_t done = atomicAdd(p.hdr + 1, 1u);
+      if (done == s.g - 1) {
+        p.hdr[1] = 0u;
+        __threadfence();
+        p.hdr[0] = epoch;
+      }
+    }
   }
 
   tc_fence_before();
@@ -516,21 +727,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t inner,
-                    uint64_t outer, uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
-                    CUtensorMapSwizzle swz) {
+static int make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, uint32_t esize,
+                    uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_inner,
+                    uint32_t box_outer, CUtensorMapSwizzle swz) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
     return SKPP_ELAUNCH;
   }
   const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {ld_elems * 2};
+  const cuuint64_t strides[1] = {ld_elems * esize};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, dtype == SKPP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                  2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -540,7 +749,13 @@ static int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t inne
   return SKPP_OK;
 }
 
-static bool sched_from_c(const skpp_sched_t& c, Sched& s) {
+static CUtensorMapDataType map_dtype(int d) {
+  return d == SKPP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+         : d == SKPP_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+}
+
+static void sched_from_c(const skpp_sched_t& c, Sched& s) {
   s.dp_tiles = c.dp_tiles;
   s.sk_tiles = c.sk_tiles;
   s.ipt = c.iters_per_tile;
@@ -549,12 +764,43 @@ static bool sched_from_c(const skpp_sched_t& c, Sched& s) {
   s.n_tiles = c.n_tiles;
   s.g = c.g;
   s.sk_first = c.sk_first;
-  return true;
+}
+
+static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
+static uint32_t g_l2_prefetch = 0;       // skpp_set_l2_prefetch
+
+// A prepared launch: tensor maps, parameters and kernel, built once.
+struct Plan {
+  const void* func;
+  uint32_t smem;
+  uint32_t block_n;
+  CUtensorMap ma, mb, mc;
+  GemmParams p;
+  skpp_sched_t cs;
+  uint64_t ws_bytes;
+  void* ws_bound;   // workspace the parameters point into
+};
+
+template <int BN, int BK>
+static int kernel_setup(const void** func, uint32_t* smem) {
+  using C = Cfg<BN, BK>;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  });
+  if (err != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
+    return SKPP_ELAUNCH;
+  }
+  *func = reinterpret_cast<const void*>(streamk_gemm_kernel<BN, BK>);
+  *smem = C::SMEM;
+  return SKPP_OK;
 }
 
 template <int BN, int BK>
 static int max_coresident_impl(int* ctas) {
-  using C = Cfg<BN, BK>;
   constexpr int kMaxDev = 64;
   static int cache[kMaxDev] = {0};  // 0 = not yet queried
   int cur = 0;
@@ -563,17 +809,14 @@ static int max_coresident_impl(int* ctas) {
     *ctas = cache[cur];
     return SKPP_OK;
   }
-  auto kern = streamk_gemm_kernel<BN, BK>;
+  const void* func;
+  uint32_t smem;
+  int rc = kernel_setup<BN, BK>(&func, &smem);
+  if (rc) return rc;
+  int per_sm = 0, sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur);
   cudaError_t e =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-  if (e != cudaSuccess) {
-    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    return SKPP_ELAUNCH;
-  }
-  int per_sm = 0, dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, C::SMEM);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, streamk_gemm_kernel<BN, BK>, kThreads, smem);
   if (e != cudaSuccess) {
     set_error(std::string("occupancy query: ") + cudaGetErrorString(e));
     return SKPP_ELAUNCH;
@@ -583,86 +826,14 @@ static int max_coresident_impl(int* ctas) {
   return SKPP_OK;
 }
 
-template <int BN, int BK>
-static int launch_impl(const skpp_sched_t& cs, uint64_t M, uint64_t N, uint64_t K,
-                       const skpp_operands_t& ops, void* ws, int64_t* trace, uint64_t trace_cap,
-                       int64_t* trace_counts, cudaStream_t stream) {
-  using C = Cfg<BN, BK>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-  });
-  if (attr_err != cudaSuccess) {
-    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-    return SKPP_ELAUNCH;
-  }
-  CUtensorMap ma, mb;
-  const CUtensorMapSwizzle aswz = BK == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
-                                  : BK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                             : CU_TENSOR_MAP_SWIZZLE_32B;
-  int rc = make_map(&ma, ops.a, ops.in_dtype, K, M, (uint64_t)ops.lda, BK, kBM, aswz);
-  if (rc) return rc;
-  rc = make_map(&mb, ops.b, ops.in_dtype, N, K, (uint64_t)ops.ldb, 64, BK,
-                CU_TENSOR_MAP_SWIZZLE_128B);
-  if (rc) return rc;
-
-  GemmParams p;
-  memset(&p, 0, sizeof(p));
-  sched_from_c(cs, p.s);
-  p.M = (uint32_t)M;
-  p.N = (uint32_t)N;
-  const uint32_t ab = ops.in_dtype == SKPP_BF16 ? 1u : 0u;
-  p.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (0u << 15) | (1u << 16) |
-            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
-  p.out_dtype = ops.out_dtype;
-  p.C = ops.c;
-  p.ldc = (uint64_t)ops.ldc;
-  const uint64_t esz = ops.out_dtype == SKPP_F32 ? 4 : 2;
-  p.c_vec_ok = ((reinterpret_cast<uintptr_t>(ops.c) % 16) == 0 && (p.ldc * esz) % 16 == 0) ? 1 : 0;
-  p.ws = reinterpret_cast<float*>(ws);
-  p.flags = ws ? reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(ws) +
-                                             (uint64_t)cs.g * kBM * BN * 4)
-               : nullptr;
-  p.trace = trace;
-  p.trace_cap = trace_cap;
-  p.trace_counts = trace_counts;
-
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(cs.g);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  int nattr = 0;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(stream, &cap);
-  if (cs.sk_tiles > 0 && cap == cudaStreamCaptureStatusNone) {
-    // Stream-K owners spin on peers: every CTA must be resident at once.
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    nattr = 1;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = nattr;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, streamk_gemm_kernel<BN, BK>, ma, mb, p);
-  if (e != cudaSuccess) {
-    set_error(std::string("GEMM launch failed: ") + cudaGetErrorString(e));
-    return SKPP_ELAUNCH;
-  }
-  return SKPP_OK;
-}
-
 // Calls f(integral_constant<BN>, integral_constant<BK>) for the instantiated tile shapes.
 template <typename F>
 static int dispatch_tile(const skpp_tile_t* t, F&& f) {
+  using I16 = std::integral_constant<int, 16>;
+  using I32 = std::integral_constant<int, 32>;
   using I64 = std::integral_constant<int, 64>;
   using I128 = std::integral_constant<int, 128>;
   using I256 = std::integral_constant<int, 256>;
-  using I32 = std::integral_constant<int, 32>;
-  using I16 = std::integral_constant<int, 16>;
   if (t->blk_m != (uint32_t)kBM) return SKPP_ETILE;
   if (t->blk_k == 64) {
     if (t->blk_n == 64) return f(I64{}, I64{});
@@ -678,6 +849,27 @@ static int dispatch_tile(const skpp_tile_t* t, F&& f) {
     if (t->blk_n == 256) return f(I256{}, I16{});
   }
   return SKPP_ETILE;
+}
+
+static int check_device() {
+  constexpr int kMaxDev = 64;
+  static int verified[kMaxDev] = {0};  // 1 = sm_100 checked
+  int dev = 0, major = 0, minor = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    set_error(std::string("no CUDA device: ") + cudaGetErrorString(e));
+    return SKPP_EARCH;
+  }
+  if (dev >= 0 && dev < kMaxDev && verified[dev]) return SKPP_OK;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) {
+    set_error("libskpp kernels are built for sm_100a (B200); device is sm_" +
+              std::to_string(major) + std::to_string(minor));
+    return SKPP_EARCH;
+  }
+  if (dev >= 0 && dev < kMaxDev) verified[dev] = 1;
+  return SKPP_OK;
 }
 
 }  // namespace skpp
@@ -696,10 +888,11 @@ extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_til
                                          uint32_t g) {
   (void)p;
   if (!t) return 0;
-  const uint64_t part = (uint64_t)g * t->blk_m * t->blk_n * 4;
-  const uint64_t flags = (((uint64_t)g * 4) + 255) / 256 * 256;
-  return part + flags;
+  return kWsHeader + ws_flag_bytes(g) + 2ull * g * t->blk_m * t->blk_n * 4;
 }
+
+extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
+extern "C" void skpp_set_l2_prefetch(uint32_t k_blocks) { g_l2_prefetch = k_blocks; }
 
 extern "C" int skpp_set_device(int device) {
   cudaError_t e = cudaSetDevice(device);
@@ -743,31 +936,15 @@ extern "C" int skpp_max_coresident(const skpp_tile_t* t, int32_t* ctas) {
   return rc;
 }
 
-static int check_device() {
-  int dev = 0, major = 0, minor = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) {
-    set_error(std::string("no CUDA device: ") + cudaGetErrorString(e));
-    return SKPP_EARCH;
-  }
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-  if (major != 10 || minor != 0) {
-    set_error("libskpp kernels are built for sm_100a (B200); device is sm_" +
-              std::to_string(major) + std::to_string(minor));
-    return SKPP_EARCH;
-  }
-  return SKPP_OK;
-}
-
-extern "C" int skpp_gemm_launch(const skpp_problem_t* p, const skpp_tile_t* t,
+extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
                                 const skpp_policy_t* pol, uint32_t g, const skpp_operands_t* ops,
-                                void* workspace, uint64_t workspace_bytes, int64_t* trace,
-                                uint64_t trace_cap, int64_t* trace_counts, void* stream) {
-  if (!p || !t || !pol || !ops) {
+                                int64_t* trace, uint64_t trace_cap, int64_t* trace_counts,
+                                void** plan_out) {
+  if (!p || !t || !pol || !ops || !plan_out) {
     set_error("null argument");
     return SKPP_EINVAL;
   }
+  *plan_out = nullptr;
   if (!skpp_tile_supported(t)) {
     set_error("tile shape " + std::to_string(t->blk_m) + "x" + std::to_string(t->blk_n) + "x" +
               std::to_string(t->blk_k) +
@@ -805,29 +982,145 @@ extern "C" int skpp_gemm_launch(const skpp_problem_t* p, const skpp_tile_t* t,
   }
   int rc = check_device();
   if (rc) return rc;
-  skpp_sched_t cs;
-  rc = skpp_sched_make(p, t, g, pol, &cs);
-  if (rc) return rc;
-  if (cs.sk_tiles > 0) {
-    if (workspace_bytes < skpp_workspace_bytes(p, t, g) || workspace == nullptr) {
-      set_error("workspace too small: need " + std::to_string(skpp_workspace_bytes(p, t, g)) +
-                " bytes");
-      return SKPP_EWORKSPACE;
-    }
+  Plan* pl = new Plan;
+  memset(pl, 0, sizeof(Plan));
+  rc = skpp_sched_make(p, t, g, pol, &pl->cs);
+  if (rc) {
+    delete pl;
+    return rc;
+  }
+  if (pl->cs.sk_tiles > 0) {
     int co = 0;
     rc = max_coresident_dispatch(t, &co);
-    if (rc) return rc;
+    if (rc) {
+      delete pl;
+      return rc;
+    }
     if ((int64_t)g > co) {
       set_error("g=" + std::to_string(g) + " exceeds the " + std::to_string(co) +
                 " co-resident CTAs the Stream-K fixup needs");
+      delete pl;
       return SKPP_EGRID;
     }
   }
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return dispatch_tile(t, [&](auto bn, auto bk) {
-    return launch_impl<decltype(bn)::value, decltype(bk)::value>(
-        cs, p->m, p->n, p->k, *ops, workspace, trace, trace_cap, trace_counts, st);
+  rc = dispatch_tile(t, [&](auto bn, auto bk) {
+    return kernel_setup<decltype(bn)::value, decltype(bk)::value>(&pl->func, &pl->smem);
   });
+  if (rc) {
+    delete pl;
+    return rc;
+  }
+  pl->block_n = t->blk_n;
+  const uint32_t BK = t->blk_k;
+  const CUtensorMapSwizzle aswz = BK == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : BK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                             : CU_TENSOR_MAP_SWIZZLE_32B;
+  const CUtensorMapDataType in_dt = map_dtype(ops->in_dtype);
+  rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK, kBM, aswz);
+  if (!rc)
+    rc = make_map(&pl->mb, ops->b, in_dt, 2, p->n, p->k, (uint64_t)ops->ldb, 64, BK,
+                  CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) {
+    delete pl;
+    return rc;
+  }
+  GemmParams& gp = pl->p;
+  sched_from_c(pl->cs, gp.s);
+  gp.M = (uint32_t)p->m;
+  gp.N = (uint32_t)p->n;
+  const uint32_t ab = ops->in_dtype == SKPP_BF16 ? 1u : 0u;
+  gp.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (0u << 15) | (1u << 16) |
+             ((uint32_t)(t->blk_n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+  gp.out_dtype = ops->out_dtype;
+  gp.C = ops->c;
+  gp.ldc = (uint64_t)ops->ldc;
+  const uint32_t esz = ops->out_dtype == SKPP_F32 ? 4 : 2;
+  gp.c_vec_ok = ((reinterpret_cast<uintptr_t>(ops->c) % 16) == 0 && (gp.ldc * esz) % 16 == 0) ? 1 : 0;
+  if (gp.c_vec_ok) {
+    rc = make_map(&pl->mc, ops->c, map_dtype(ops->out_dtype), esz, p->n, p->m, gp.ldc,
+                  128 / esz, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) {
+      delete pl;
+      return rc;
+    }
+    gp.c_tma = 1;
+  }
+  gp.trace = trace;
+  gp.trace_cap = trace_cap;
+  gp.trace_counts = trace_counts;
+  pl->ws_bytes = pl->cs.sk_tiles ? skpp_workspace_bytes(p, t, g) : 0;
+  *plan_out = pl;
+  return SKPP_OK;
+}
+
+extern "C" uint64_t skpp_plan_workspace_bytes(const void* plan) {
+  return plan ? static_cast<const Plan*>(plan)->ws_bytes : 0;
+}
+
+extern "C" void skpp_plan_destroy(void* plan) { delete static_cast<Plan*>(plan); }
+
+extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_bytes,
+                                void* stream) {
+  Plan* pl = static_cast<Plan*>(plan);
+  if (!pl) {
+    set_error("null plan");
+    return SKPP_EINVAL;
+  }
+  GemmParams& gp = pl->p;
+  if (pl->cs.sk_tiles > 0) {
+    if (workspace == nullptr || workspace_bytes < pl->ws_bytes) {
+      set_error("workspace too small: need " + std::to_string(pl->ws_bytes) + " bytes");
+      return SKPP_EWORKSPACE;
+    }
+    if (pl->ws_bound != workspace) {
+      uint8_t* base = reinterpret_cast<uint8_t*>(workspace);
+      gp.hdr = reinterpret_cast<uint32_t*>(base);
+      gp.flags = reinterpret_cast<uint32_t*>(base + kWsHeader);
+      gp.ws = reinterpret_cast<float*>(base + kWsHeader + ws_flag_bytes(pl->cs.g));
+      pl->ws_bound = workspace;
+    }
+  }
+  gp.timeline = g_timeline;
+  gp.l2_prefetch = g_l2_prefetch;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(pl->cs.g);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl->smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 0;
+  if (pl->cs.sk_tiles > 0) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (cap == cudaStreamCaptureStatusNone) {
+      // Stream-K contributors wait on each other: every CTA must be resident at once.
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.numAttrs = 1;
+    }
+  }
+  void* args[4] = {&pl->ma, &pl->mb, &pl->mc, &gp};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, pl->func, args);
+  if (e != cudaSuccess) {
+    set_error(std::string("GEMM launch failed: ") + cudaGetErrorString(e));
+    return SKPP_ELAUNCH;
+  }
+  return SKPP_OK;
+}
+
+extern "C" int skpp_gemm_launch(const skpp_problem_t* p, const skpp_tile_t* t,
+                                const skpp_policy_t* pol, uint32_t g, const skpp_operands_t* ops,
+                                void* workspace, uint64_t workspace_bytes, int64_t* trace,
+                                uint64_t trace_cap, int64_t* trace_counts, void* stream) {
+  void* plan = nullptr;
+  int rc = skpp_plan_create(p, t, pol, g, ops, trace, trace_cap, trace_counts, &plan);
+  if (rc) return rc;
+  rc = skpp_plan_launch(plan, workspace, workspace_bytes, stream);
+  skpp_plan_destroy(plan);
+  return rc;
 }
 
 extern "C" int skpp_schedule_trace_device(const skpp_problem_t* p, const skpp_tile_t* t,

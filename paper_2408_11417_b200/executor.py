@@ -133,8 +133,11 @@ def tile_supported(tile: TileShape) -> bool:
 def workspace_for(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
     """Zero-initialised fixup workspace, cached per (device, stream).
 
-    The kernel returns every flag to zero when it completes, so a cached
-    buffer can be reused by the next launch on the same stream.
+    The kernel keeps the workspace consistent itself (flags are tagged with
+    an epoch stored in the workspace header and advanced by the last CTA of
+    each launch), so a cached buffer serves every later launch on the same
+    stream, graph replays included.  Plans hold a reference to the buffer
+    they were bound to, so growing the cache never frees memory in use.
     """
     key = (device, stream_handle)
     with _ws_lock:
@@ -149,8 +152,9 @@ def workspace_for(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
 class GemmPlan:
     """A prepared launch: C = A @ B under one policy, reusable and graph-capturable.
 
-    All ctypes structures are built once; :meth:`launch` is a single call into
-    ``skpp_gemm_launch`` on the current stream.
+    The schedule scalars, kernel choice and TMA descriptors are built once in
+    C++ (``skpp_plan_create``); :meth:`launch` binds the per-stream workspace
+    and makes a single ``skpp_plan_launch`` call on the current stream.
     """
 
     def __init__(
@@ -190,25 +194,11 @@ class GemmPlan:
         self.tile = tile
         self.policy = policy
         self.g = sm_count(dev) if g is None else int(g)
-        self.a, self.b, self.c = a, b, c
+        self.a, self.b, self.c = a, b, c  # keep the operands alive as long as the plan
         self.device = dev
-        self._problem = _lib.Problem(m, n, k)
-        self._tile = _lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k)
         self.sched_c = closed_form(self.size, tile, self.g, policy)
         from .scheduler import policy_to_c
 
-        self._policy = policy_to_c(policy)
-        self._ops = _lib.Operands(
-            a.data_ptr(),
-            a.stride(0),
-            b.data_ptr(),
-            b.stride(0),
-            c.data_ptr(),
-            c.stride(0),
-            _IN_DTYPES[a.dtype],
-            _OUT_DTYPES[c.dtype],
-        )
-        self.ws_bytes = int(_lib.lib.skpp_workspace_bytes(self._problem, self._tile, self.g))
         self.trace_cap = int(trace_cap)
         if self.trace_cap:
             self.trace = torch.full(
@@ -217,33 +207,50 @@ class GemmPlan:
             self.trace_counts = torch.zeros(self.g, dtype=torch.int64, device=a.device)
         else:
             self.trace = self.trace_counts = None
+        ops = _lib.Operands(
+            a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), c.data_ptr(), c.stride(0),
+            _IN_DTYPES[a.dtype], _OUT_DTYPES[c.dtype],
+        )
+        handle = ctypes.c_void_p()
+        rc = _lib.lib.skpp_plan_create(
+            _lib.Problem(m, n, k), _lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k), policy_to_c(policy),
+            self.g, ops,
+            self.trace.data_ptr() if self.trace is not None else None, self.trace_cap,
+            self.trace_counts.data_ptr() if self.trace_counts is not None else None,
+            ctypes.byref(handle),
+        )
+        if rc != _lib.OK:
+            msg = _lib.last_error()
+            if rc in (_lib.ETILE, _lib.EALIGN, _lib.EINVAL, _lib.EGRID):
+                raise ValueError(msg)
+            raise _lib.SkppError(rc, msg)
+        self._handle = handle.value
+        self.ws_bytes = int(_lib.lib.skpp_plan_workspace_bytes(self._handle))
+        self._launch = _lib.lib.skpp_plan_launch
+        self._ws_cache: dict[int, tuple] = {}
+
+    def __del__(self):
+        h, self._handle = getattr(self, "_handle", None), None
+        if h:
+            _lib.lib.skpp_plan_destroy(h)
 
     @property
     def uses_fixup(self) -> bool:
         return self.sched_c.sk_tiles > 0
 
     def launch(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-        st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        handle = st.cuda_stream
-        ws = workspace_for(self.ws_bytes, self.device, handle) if self.uses_fixup else None
-        rc = _lib.lib.skpp_gemm_launch(
-            self._problem,
-            self._tile,
-            self._policy,
-            self.g,
-            self._ops,
-            ws.data_ptr() if ws is not None else None,
-            self.ws_bytes if ws is not None else 0,
-            self.trace.data_ptr() if self.trace is not None else None,
-            self.trace_cap,
-            self.trace_counts.data_ptr() if self.trace_counts is not None else None,
-            handle,
-        )
+        handle = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(self.device)
+        ws = self._ws_cache.get(handle)
+        if ws is None:
+            if self.ws_bytes:
+                buf = workspace_for(self.ws_bytes, self.device, handle)
+                ws = (buf.data_ptr(), buf.numel(), buf)
+            else:
+                ws = (None, 0, None)
+            self._ws_cache[handle] = ws
+        rc = self._launch(self._handle, ws[0], ws[1], handle)
         if rc != _lib.OK:
-            msg = _lib.last_error()
-            if rc in (_lib.ETILE, _lib.EALIGN, _lib.EINVAL, _lib.EGRID, _lib.EWORKSPACE):
-                raise ValueError(msg)
-            raise _lib.SkppError(rc, msg)
+            raise _lib.SkppError(rc, _lib.last_error())
         return self.c
 
     def trace_items(self) -> list[list[tuple[int, int, int, int, int, int]]]:
@@ -335,10 +342,13 @@ def execute_schedule(
     _check_closed_form(sched, size, tile)
 
     dev = _require_cuda()
+    host_result = False
     if is_torch:
         if not a.is_cuda:
-            a = a.cuda()
-            b = b.cuda()
+            # Host tensors (ideally pinned): copy in, and hand the result back on the host.
+            host_result = True
+            a = a.to(f"cuda:{dev}", non_blocking=True)
+            b = b.to(f"cuda:{dev}", non_blocking=True)
         op_dtype = a.dtype if a.dtype in _IN_DTYPES else _as_dtype(in_dtype, torch.bfloat16)
         res_dtype = _as_dtype(out_dtype, torch.float32)
         ad = a.to(op_dtype)
@@ -362,7 +372,7 @@ def execute_schedule(
     GemmPlan(ad, bd, c, sched.policy, tile, sched.g).launch()
     out = c[:, : size.n]
     if is_torch:
-        return out
+        return out.cpu() if host_result else out
     return out.to(torch.float64).cpu().numpy()
 
 

@@ -1,0 +1,303 @@
+"""Product host path (libskpp.so through the Python API) vs golden vectors and the oracle (CPU).
+
+Bit-exact: murmur/hash24, filter sizing, seeds, probes, Bloom bits, bank
+bytes, query answers, parse errors (class and order), schedules item for
+item, coverage audits, elimination statistics and the ranking tie-break.
+"""
+
+import hashlib
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+import paper_2408_11417_b200 as sk
+from paper_2408_11417_b200 import hashing as sh
+from paper_2408_11417_b200 import sieve as ss
+from oracle import schedule as osc
+from oracle import sieve as osv
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+CANON = sk.canonical_policies()
+
+
+def pol(t):
+    kind, s, first = t
+    if kind == "data-parallel":
+        return sk.Policy.data_parallel()
+    if kind == "all-streamk":
+        return sk.Policy.all_stream_k()
+    return sk.Policy.hybrid(s, first)
+
+
+def rows_of(sched):
+    return [[[it.tile_idx, it.local_iter_begin, it.local_iter_end,
+              0 if it.write_mode is sk.WriteMode.FULL_STORE else 1,
+              0 if it.phase is sk.Phase.STREAM_K else 1] for it in wg] for wg in sched.assignments]
+
+
+def digest(rows):
+    txt = "|".join(";".join(",".join(str(v) for v in item) for item in wg) for wg in rows)
+    return hashlib.sha256(txt.encode()).hexdigest()
+
+
+# -- hashing -----------------------------------------------------------------
+
+
+def test_murmur_kats_and_random():
+    for lit, seed, want in GOLD["kat"]["murmur"]:
+        assert list(sh.murmur3_x64_128(lit.encode(), seed)) == want
+    for hexdata, seed, want in GOLD["murmur_random"]:
+        assert list(sh.murmur3_x64_128(bytes.fromhex(hexdata), seed)) == want
+
+
+def test_smhasher_verification_value():
+    buf = bytearray()
+    for i in range(256):
+        h1, h2 = sh.murmur3_x64_128(bytes(range(i)), 256 - i)
+        buf += struct.pack("<QQ", h1, h2)
+    assert sh.murmur3_x64_128(bytes(buf), 0)[0] & 0xFFFFFFFF == 0x6384BA69
+
+
+def test_hash24_matches_general_murmur():
+    for (m, n, k), seed, want in GOLD["kat"]["triple"] + GOLD["hash24"]:
+        assert list(sh.hash24(m, n, k, seed)) == want
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        m, n, k = (int(v) for v in rng.integers(1, 2**63, size=3, dtype=np.uint64))
+        seed = int(rng.integers(0, 2**32))
+        assert sh.hash24(m, n, k, seed) == sh.murmur3_x64_128(struct.pack("<QQQ", m, n, k), seed)
+
+
+def test_key_encoding():
+    assert sk.encode_key(sk.ProblemSize(256, 512, 128)).hex() == GOLD["kat"]["key_256_512_128_hex"]
+    assert sk.KEY_BYTES == 24
+
+
+# -- filters -----------------------------------------------------------------
+
+
+def test_filter_params_and_seeds():
+    for cap, fp, mb, kh in GOLD["kat"]["filter_params"] + GOLD["filter_params"]:
+        assert sk.filter_params(cap, fp) == (mb, kh)
+    assert [sk.filter_seed(i) for i in range(16)] == GOLD["filter_seeds"]
+    with pytest.raises(ValueError):
+        sk.filter_params(0, 0.01)
+    with pytest.raises(ValueError):
+        sk.filter_params(10, 1.0)
+
+
+def test_probes():
+    for (m, n, k), seed, mb, kh, want in GOLD["probes"]:
+        assert sk.hash_probes(sk.encode_key(sk.ProblemSize(m, n, k)), seed, mb, kh) == want
+    with pytest.raises(ValueError):
+        sk.hash_probes(b"short", 0, 64, 1)
+
+
+def test_bloom_bits_lsb_first_and_no_false_negatives():
+    f = sk.BloomFilter(64, 1, seed=0)
+    key = sk.encode_key(sk.ProblemSize(9, 9, 9))
+    idx = sk.hash_probes(key, 0, 64, 1)[0]
+    f.insert(key)
+    assert f.bits[idx >> 3] == 1 << (idx & 7)
+    rng = np.random.default_rng(3)
+    g = sk.BloomFilter.for_capacity(2000, 0.01, seed=7)
+    keys = [sk.encode_key(sk.ProblemSize(*(int(v) for v in rng.integers(1, 2**40, size=3)))) for _ in range(2000)]
+    for kk in keys:
+        g.insert(kk)
+    assert all(kk in g for kk in keys)
+    assert g.n_inserted == 2000
+
+
+def test_small_bank_bytes_queries_and_masks():
+    sb = GOLD["small_bank"]
+    bank = sk.SieveBank(CANON, capacity=sb["capacity"], fp_target=sb["fp_target"])
+    for (m, n, k), ordinal in sb["inserts"]:
+        bank.insert(sk.ProblemSize(m, n, k), CANON[ordinal])
+    assert bank.to_bytes().hex() == sb["hex"]
+    sizes = [sk.ProblemSize(*s) for s, _ in sb["queries"]]
+    for size, (_, want) in zip(sizes, sb["queries"]):
+        assert [p.ordinal for p in bank.query(size)] == want
+    masks = bank.query_masks(sizes)
+    for mask, (_, want) in zip(masks, sb["queries"]):
+        assert [i for i in range(7) if int(mask) >> i & 1] == want
+    # the hashing-level mask function agrees too
+    bits = np.stack([f.bits for _, f in bank.filters])
+    seeds = np.array([f.seed for _, f in bank.filters], dtype=np.uint64)
+    for size, (_, want) in list(zip(sizes, sb["queries"]))[:50]:
+        m = sh.query_mask(bits, seeds, bank.m_bits, bank.k_hashes, size.m, size.n, size.k)
+        assert [i for i in range(7) if m >> i & 1] == want
+
+
+def test_bank_round_trip_and_oracle_bytes():
+    sb = GOLD["small_bank"]
+    data = bytes.fromhex(sb["hex"])
+    bank = sk.SieveBank.from_bytes(data)
+    assert bank.to_bytes() == data
+    assert bank.policies == CANON
+    ob = osv.Bank(osv.CANONICAL, sb["capacity"], sb["fp_target"])
+    for (m, n, k), ordinal in sb["inserts"]:
+        ob.insert(m, n, k, osv.CANONICAL[ordinal])
+    assert ob.to_bytes() == data
+
+
+def test_parse_errors_follow_reference_order():
+    classes = {
+        None: None,
+        "TruncatedError": sk.TruncatedError,
+        "BadMagicError": sk.BadMagicError,
+        "UnsupportedVersionError": ss.UnsupportedVersionError,
+        "SieveFormatError": sk.SieveFormatError,
+        "ChecksumError": sk.ChecksumError,
+    }
+    for label, hexdata, err in GOLD["parse_cases"]:
+        data = bytes.fromhex(hexdata)
+        if err is None:
+            sk.SieveBank.from_bytes(data)
+            continue
+        with pytest.raises(sk.SieveFormatError) as info:
+            sk.SieveBank.from_bytes(data)
+        assert type(info.value) is classes[err], (label, type(info.value).__name__, err)
+
+
+def test_every_single_byte_flip_is_detected():
+    data = bytes.fromhex(GOLD["small_bank"]["hex"])
+    rng = np.random.default_rng(0)
+    for pos in rng.choice(len(data), size=300, replace=False):
+        bad = bytearray(data)
+        bad[int(pos)] ^= 1 << int(rng.integers(0, 8))
+        with pytest.raises(ValueError):
+            sk.SieveBank.from_bytes(bytes(bad))
+
+
+def test_default_tune_bank_from_reference_winners():
+    """Reference cost-model winners -> our build_bank -> the reference's CLI artefact bytes."""
+    dt = GOLD["default_tune"]
+    grid = sk.gen_problem_grid(sk.DEFAULT_GRID)
+    assert len(grid) == dt["grid_len"]
+    assert [grid[0].m, grid[0].n, grid[0].k] == dt["first"]
+    assert [grid[-1].m, grid[-1].n, grid[-1].k] == dt["last"]
+    est = sk.CostEstimate(1.0, 1.0, 0, 0)
+    recs = [sk.TuneRecord(s, (), CANON[w], CANON[w], 0.0) for s, w in zip(grid, dt["winners"])]
+    rng = np.random.default_rng(1)
+    shuffled = [recs[i] for i in rng.permutation(len(recs))]
+    bank = sk.build_bank(shuffled)
+    data = bank.to_bytes()
+    assert len(data) == dt["bank_bytes"]
+    assert hashlib.sha256(data).hexdigest() == dt["bank_sha256"]
+    el = sk.elimination_stats(bank, recs)
+    assert [el.eliminated_fraction, el.false_negatives, el.evaluations_saved] == dt["elimination"]
+    for s, want in zip(grid[:200], dt["query_masks_first_200"]):
+        assert [p.ordinal for p in bank.query(s)] == want
+    del est
+
+
+def test_ranking_tie_break():
+    for costs, win, run in GOLD["ranking"]:
+        rec = sk.rank_costs(sk.ProblemSize(1, 1, 1),
+                            [(p, sk.CostEstimate(c, 0.0, 0, 0)) for p, c in zip(CANON, costs)])
+        assert (rec.winner.ordinal, rec.runner_up.ordinal) == (win, run)
+
+
+# -- schedules ---------------------------------------------------------------
+
+
+def test_schedules_match_reference_golden():
+    for rec in GOLD["schedules"]:
+        s = sk.build_schedule(sk.ProblemSize(*rec["size"]), sk.TileShape(*rec["tile"]),
+                              sk.HardwareModel(rec["g"], 1), pol(rec["policy"]))
+        rows = rows_of(s)
+        assert sum(len(w) for w in rows) == rec["n_items"]
+        assert digest(rows) == rec["digest"], rec
+        if "items" in rec:
+            assert rows == rec["items"]
+        assert sk.validate_schedule(s).covered_once
+
+
+def test_schedules_match_oracle_random():
+    rng = np.random.default_rng(11)
+    pols = CANON + [sk.Policy.hybrid(2, False), sk.Policy.hybrid(9), sk.Policy.hybrid(4, False)]
+    for i in range(300):
+        m, n, k = (int(2 ** rng.uniform(0, 13)) for _ in range(3))
+        bm, bn = (int(rng.choice([16, 32, 64, 128, 256])) for _ in range(2))
+        bk = int(rng.choice([8, 16, 32, 64]))
+        g = int(rng.integers(1, 600))
+        p = pols[i % len(pols)]
+        got = rows_of(sk.build_schedule(sk.ProblemSize(m, n, k), sk.TileShape(bm, bn, bk), sk.HardwareModel(g, 1), p))
+        want = osc.build_schedule(m, n, k, bm, bn, bk, g, p.kind.value, p.sk_batches, p.sk_first)
+        assert got == [[list(it) for it in wg] for wg in want], (m, n, k, bm, bn, bk, g, p)
+
+
+def test_fixup_roles_and_ownership_invariants():
+    """Every split tile: one owner (kb == 0), peers = the next CTAs, <= 1 peer partial per CTA."""
+    from paper_2408_11417_b200 import scheduler as ps
+
+    rng = np.random.default_rng(2)
+    for i in range(200):
+        m, n, k = (int(2 ** rng.uniform(0, 13)) for _ in range(3))
+        g = int(rng.integers(1, 300))
+        p = CANON[i % 7]
+        sc = ps.closed_form(sk.ProblemSize(m, n, k), sk.TileShape(128, 128, 64), g, p)
+        items, offsets = ps.schedule_arrays(sc)
+        want_roles = osc.fixup_roles(
+            osc.build_schedule(m, n, k, 128, 128, 64, g, p.kind.value, p.sk_batches, p.sk_first), int(sc.iters_per_tile))
+        got_roles = [items[offsets[x]:offsets[x + 1], 5].tolist() for x in range(g)]
+        assert got_roles == want_roles
+        contributors: dict[int, list[int]] = {}
+        for x in range(g):
+            peers = 0
+            for row in items[offsets[x]:offsets[x + 1]]:
+                if row[3] == 1:
+                    contributors.setdefault(int(row[0]), []).append(x)
+                    peers += row[5] == 2
+            assert peers <= 1
+        for tile, xs in contributors.items():
+            assert xs == list(range(xs[0], xs[0] + len(xs)))
+
+
+def test_coverage_audit_matches_reference():
+    for rec in GOLD["coverage"]:
+        mt, nt, ipt, tt, ti = rec["grid"]
+        grid = sk.GridInfo(mt, nt, ipt, tt, ti)
+        items = tuple(tuple(sk.WorkItem(t, kb, ke, sk.WriteMode.FULL_STORE if wm == 0 else sk.WriteMode.ATOMIC_PARTIAL,
+                                        sk.Phase.STREAM_K if ph == 0 else sk.Phase.DATA_PARALLEL)
+                            for t, kb, ke, wm, ph in wg) for wg in rec["items"])
+        rep = sk.validate_schedule(sk.Schedule(grid, rec["g"], pol(rec["policy"]), items))
+        assert [rep.covered_once, rep.duplicates, rep.gaps] == rec["report"]
+
+
+def test_grid_helpers_reference_examples():
+    # tests/test_scheduler.py examples (reference)
+    assert sk.streamk_ranges(64, 5)[0] == (0, 13)
+    assert sk.streamk_ranges(10, 4) == [(0, 3), (3, 6), (6, 9), (9, 10)]
+    assert sk.streamk_ranges(2, 4) == [(0, 1), (1, 2), (2, 2), (2, 2)]
+    gi = sk.grid_info(sk.ProblemSize(100, 100, 100), sk.TileShape(32, 32, 32))
+    assert (gi.m_tiles, gi.n_tiles, gi.iters_per_tile, gi.total_tiles, gi.total_iters) == (4, 4, 4, 16, 64)
+    assert tuple(sk.locate_iter(9, sk.GridInfo(2, 3, 4, 6, 24))) == (2, 0, 2, 1)
+    assert sk.hybrid_sk_tiles(32, 5, 1) == 2
+    assert sk.hybrid_sk_tiles(30, 5, 1) == 5
+    assert sk.hybrid_sk_tiles(30, 5, 9) == 30
+    with pytest.raises(ValueError):
+        sk.grid_info(sk.ProblemSize(2**63, 2**63, 2**63), sk.TileShape(1, 1, 1))
+    with pytest.raises(ValueError):
+        sk.locate_iter(24, sk.GridInfo(2, 3, 4, 6, 24))
+
+
+def test_hybrid1_structure_reference_example():
+    # tests/test_scheduler.py:186-205: T=32, g=5 -> SK tiles {30, 31}, 8 iters each CTA... DP 30 tiles
+    s = sk.build_schedule(sk.ProblemSize(32 * 16, 16, 16 * 8), sk.TileShape(16, 16, 16), sk.HardwareModel(5, 1),
+                          sk.Policy.hybrid(1))
+    sk_tiles = {it.tile_idx for it in s.items() if it.phase is sk.Phase.STREAM_K}
+    dp_tiles = [it.tile_idx for it in s.items() if it.phase is sk.Phase.DATA_PARALLEL]
+    assert sk_tiles == {30, 31}
+    assert sorted(dp_tiles) == list(range(30))
+    wg0 = [it.tile_idx for it in s.assignments[0] if it.phase is sk.Phase.DATA_PARALLEL]
+    assert wg0 == [0, 5, 10, 15, 20, 25]
+
+
+def test_dp_utilization():
+    assert sk.dp_utilization(sk.GridInfo(1, 105, 1, 105, 105), 104) == pytest.approx(105 / 208)
+    with pytest.raises(ValueError):
+        sk.dp_utilization(sk.GridInfo(0, 0, 1, 0, 0), 104)

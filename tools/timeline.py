@@ -1,0 +1,73 @@
+#!/usr/bin/env python
+"""Per-CTA phase timeline of one Stream-K++ launch (skpp_debug_timeline, %globaltimer ns)."""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+EVENTS = ["start", "first_tma", "first_full", "mma_done", "phase1", "waited", "phase2", "-", "epi_first", "part_issued", "part_flag"]
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=512)
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--k", type=int, default=16384)
+    ap.add_argument("--tile", default="128x128x64")
+    ap.add_argument("--policy", default="ask")
+    ap.add_argument("--flush", action="store_true")
+    ap.add_argument("--per-cta", type=int, default=0, help="print the first N CTAs")
+    ap.add_argument("--prefetch", type=int, default=0, help="L2 prefetch depth (k-blocks)")
+    args = ap.parse_args()
+
+    import torch
+
+    import paper_2408_11417_b200 as sk
+    from paper_2408_11417_b200 import _lib
+    from tools.profile_gemm import parse_policy
+
+    tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
+    a = torch.randn(args.m, args.k, device="cuda").to(torch.bfloat16)
+    b = torch.randn(args.k, args.n, device="cuda").to(torch.bfloat16)
+    c = torch.empty(args.m, args.n, device="cuda")
+    _lib.lib.skpp_set_l2_prefetch(args.prefetch)
+    plan = sk.GemmPlan(a, b, c, parse_policy(sk, args.policy), tile)
+    tl = torch.zeros(plan.g * 16, dtype=torch.int64, device="cuda")
+    flush = torch.empty(64 << 20, device="cuda")
+    for _ in range(3):
+        plan.launch()
+    if args.flush:
+        flush.zero_()
+        flush.sum()
+    torch.cuda.synchronize()
+    _lib.lib.skpp_debug_timeline(tl.data_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    plan.launch()
+    e1.record()
+    torch.cuda.synchronize()
+    _lib.lib.skpp_debug_timeline(None)
+    t = tl.view(plan.g, 16).cpu().numpy().astype("float64")
+    base = t[:, 0][t[:, 0] > 0].min()
+    print(f"{args.m}x{args.n}x{args.k} {args.policy} tile {args.tile} flush={args.flush}: "
+          f"prefetch={args.prefetch} event time {e0.elapsed_time(e1) * 1e3:.1f} us, "
+          f"kernel span {(t[:, :11].max() - base) / 1e3:.2f} us")
+    for i, name in enumerate(EVENTS):
+        if name == "-":
+            continue
+        col = t[:, i]
+        col = col[col > 0] - base
+        if len(col):
+            print(f"  {name:>10}: min {col.min() / 1e3:8.2f}  med {sorted(col)[len(col) // 2] / 1e3:8.2f}  "
+                  f"max {col.max() / 1e3:8.2f} us  (n={len(col)})")
+    for x in range(min(args.per_cta, plan.g)):
+        row = [(t[x, i] - base) / 1e3 if t[x, i] > 0 else float('nan') for i in range(7)]
+        print(f"  cta {x:3d}: " + " ".join(f"{v:7.2f}" for v in row))
+
+
+if __name__ == "__main__":
+    main()
