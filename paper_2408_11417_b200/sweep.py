@@ -93,6 +93,8 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
         t1.synchronize()
         est_us = max(t0.elapsed_time(t1) * 1e3, 1.0)
     inner = int(max(1, min(params.max_inner, params.target_us // est_us)))
+    # big problems: fewer replays (keep ~20 ms of timed work per schedule, >= 3 samples)
+    reps = int(min(params.reps, max(3, math.ceil(20000.0 / (inner * est_us)))))
     if params.use_graphs:
         graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
@@ -110,7 +112,7 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
                 plan.launch()
     torch.cuda.synchronize()
     times = []
-    for _ in range(params.reps):
+    for _ in range(reps):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -207,3 +209,142 @@ class Stopwatch:
 
     def __exit__(self, *exc):
         self.seconds = time.perf_counter() - self.t0
+
+
+# -- sharded sweep driver ---------------------------------------------------------
+
+
+def shard_path(out_dir, rank: int) -> str:
+    import os
+
+    return os.path.join(out_dir, f"records.rank{rank}.csv")
+
+
+def run_shard(sizes: list[ProblemSize], rank: int, world: int, measure, out_dir=None,
+              cost=estimated_cost_s) -> list[TuneRecord]:
+    """Measure this rank's LPT share of ``sizes`` with ``measure(sizes) -> records``.
+
+    Ranks exchange nothing on the data path: each writes its records CSV
+    shard (reference schema) and the host merges the shards afterwards.
+    """
+    from .pipeline import write_records_csv
+
+    mine = lpt_partition(sizes, world, cost)[rank]
+    mine.sort(key=lambda s: (s.m, s.n, s.k))
+    records = measure(mine) if mine else []
+    if out_dir is not None:
+        if records:
+            write_records_csv(shard_path(out_dir, rank), records)
+        else:
+            open(shard_path(out_dir, rank), "w").close()
+    return records
+
+
+def merge_shards(out_dir, world: int) -> list[TuneRecord]:
+    """Concatenate every rank's shard back into records in (m, n, k) order."""
+    import os
+
+    from .pipeline import read_records_csv, records_from_rows
+
+    rows = []
+    for r in range(world):
+        path = shard_path(out_dir, r)
+        if os.path.getsize(path) == 0:
+            continue
+        rows.extend(read_records_csv(path))
+    recs = records_from_rows(rows)
+    recs.sort(key=lambda rec: (rec.size.m, rec.size.n, rec.size.k))
+    return recs
+
+
+def gpu_measure(tile: TileShape, policies: list[Policy] | None = None, params: MeasureParams | None = None):
+    """measure(sizes) on the current GPU (one OperandPool for the whole shard)."""
+
+    def measure(sizes):
+        return tune_sizes(sizes, tile, None, policies, params)
+
+    return measure
+
+
+def main(argv=None) -> int:
+    """Sweep CLI.  Single GPU:  python -m paper_2408_11417_b200.sweep --out DIR
+    Multi GPU (one process per GPU):  torchrun --nproc-per-node N -m paper_2408_11417_b200.sweep --out DIR
+    """
+    import argparse
+    import json
+    import os
+
+    from . import pipeline as pl
+    from .sieve import elimination_stats
+
+    ap = argparse.ArgumentParser(description=main.__doc__)
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--grid", default="paper", help="paper | small | llama | paper+llama")
+    ap.add_argument("--tile", default="128x128x64")
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--max-gflop", type=float, default=0.0, help="skip sizes above this (0 = no limit)")
+    args = ap.parse_args(argv)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.makedirs(args.out, exist_ok=True)
+    sizes = grid_sizes(args.grid)
+    if args.max_gflop > 0:
+        sizes = [s for s in sizes if s.flops <= args.max_gflop * 1e9]
+    tile = TileShape(*(int(v) for v in args.tile.split("x")))
+    params = MeasureParams(warmup=args.warmup, reps=args.reps)
+    sw = Stopwatch()
+    with sw:
+        recs = run_shard(sizes, rank, world, gpu_measure(tile, None, params), args.out)
+    with open(os.path.join(args.out, f"timing.rank{rank}.json"), "w") as fh:
+        json.dump({"rank": rank, "world": world, "sizes": len(recs), "seconds": sw.seconds}, fh)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        dist.barrier()  # host-side rendezvous only: shards are files
+        dist.destroy_process_group()
+    if rank == 0:
+        merged = merge_shards(args.out, world)
+        bank = pl.build_bank(merged)
+        bank.save(os.path.join(args.out, "bank.sieve"))
+        pl.write_records_csv(os.path.join(args.out, "records.csv"), merged)
+        times = [json.load(open(os.path.join(args.out, f"timing.rank{r}.json")))["seconds"] for r in range(world)]
+        el = elimination_stats(bank, merged)
+        summary = {
+            "sizes": len(merged), "policies": 7, "tile": args.tile, "world": world,
+            "sweep_seconds_max_over_ranks": max(times),
+            "shape_policy_per_s": sweep_throughput(len(merged), 7, max(times)),
+            "winner_counts": pl.winner_counts(merged),
+            "elimination": {"eliminated_fraction": el.eliminated_fraction,
+                            "false_negatives": el.false_negatives, "evaluations_saved": el.evaluations_saved},
+            "selection": pl.selection_quality(merged, bank),
+        }
+        with open(os.path.join(args.out, "summary.json"), "w") as fh:
+            json.dump(summary, fh, indent=1)
+        print(json.dumps(summary))
+    return 0
+
+
+def grid_sizes(name: str) -> list[ProblemSize]:
+    from . import pipeline as pl
+
+    out: list[ProblemSize] = []
+    for part in name.split("+"):
+        if part == "paper":
+            out += pl.gen_problem_grid(pl.DEFAULT_GRID)
+        elif part == "small":
+            out += pl.gen_problem_grid(pl.GridSpec(pl.AxisRange(1, 1024), pl.AxisRange(64, 1024),
+                                                   pl.AxisRange(16, 4096)))
+        elif part == "llama":
+            out += pl.llama3_8b_sizes()
+        else:
+            raise ValueError(f"unknown grid {part!r}")
+    return list(dict.fromkeys(out))
+
+
+if __name__ == "__main__":  # pragma: no cover
+    raise SystemExit(main())
