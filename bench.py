@@ -49,7 +49,7 @@ WORKLOADS = {
                       "Bloom-selected policy among the 7 canonical policies"),
     "cfg1": dict(m=1024, n=1024, k=1024, dtype="fp16", tile=(128, 128, 64),
                  desc="BASELINE cfg1: fp16 GEMM 1024^3, fp32 out, Bloom-selected policy (DP vs hybrid1)"),
-    "square8192": dict(m=8192, n=8192, k=8192, dtype="bf16", tile=(128, 256, 64),
+    "square8192": dict(m=8192, n=8192, k=8192, dtype="bf16", tile=(256, 256, 64),
                        desc="large square bf16 GEMM 8192^3, fp32 out (70%-of-peak target)"),
 }
 
@@ -166,7 +166,8 @@ def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool,
     rng = np.random.default_rng(seed)
     a = ogemm.random_int_matrix(m, k, rng)
     b = ogemm.random_int_matrix(k, n, rng)
-    sched = osched.build_schedule(m, n, k, bm, bn, bk, 148, policy_kind, sk_batches, sk_first)
+    g = 148 // (bm // 128)  # one workgroup per SM, or per SM pair for 256-row tiles
+    sched = osched.build_schedule(m, n, k, bm, bn, bk, g, policy_kind, sk_batches, sk_first)
     n_tiles = -(-n // bn)
     times = []
     t_start = time.perf_counter()
@@ -239,7 +240,7 @@ def run_ours(args, wl: dict) -> None:
     in_dtype = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float16
     size = sk.ProblemSize(m, n, k)
     tile = sk.TileShape(*wl["tile"])
-    g = sk.executor.sm_count()
+    g = sk.executor.default_g(tile)
     pool = sweep.OperandPool([size], in_dtype, torch.float32, seed=rank)
     policy, rec, bank = select_policy(size, tile, g, pool)
     a, b, c = pool.views(size)

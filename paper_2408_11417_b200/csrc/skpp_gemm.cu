@@ -146,6 +146,48 @@ __device__ __forceinline__ void fence_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Both CTAs of the pair load their own smem but complete on the LEADER's barrier
+// (clearing the peer bit of the shared::cluster address selects CTA rank 0).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int32_t c0,
+                                                 int32_t c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// Arrive on the barrier at this smem offset in BOTH CTAs of the pair once the
+// pair MMAs issued so far complete.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_rank(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -187,6 +229,7 @@ __device__ __forceinline__ void tmem_ld_wait() {
 }
 
 __device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void phase2_bar_sync() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
 
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -199,6 +242,13 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 ld_cg_f4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
   return v;
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
@@ -226,10 +276,14 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int out_dtype) {
 
 // ------------------------------------------------------------ kernel config --
 
-template <int BN, int BK>
+// BN = N of the MMA (= tile width); CG = CTAs per MMA (1, or 2 for a
+// cta_group::2 pair whose tile is 256 rows: each CTA holds 128 rows of A and
+// BN/2 columns of B, and 128 accumulator lanes x BN columns of TMEM).
+template <int BN, int BK, int CG>
 struct Cfg {
+  static constexpr int BNC = BN / CG;  // B columns loaded by each CTA
   static constexpr uint32_t A_BYTES = kBM * BK * 2;
-  static constexpr uint32_t B_BYTES = BK * BN * 2;
+  static constexpr uint32_t B_BYTES = BK * BNC * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t STAGES_RAW = kRingBudget / STAGE_BYTES;
   static constexpr uint32_t STAGES = STAGES_RAW > 32 ? 32 : STAGES_RAW;
@@ -239,7 +293,7 @@ struct Cfg {
                                         : 2 * BN <= 128 ? 128
                                         : 2 * BN <= 256 ? 256
                                                         : 512;
-  static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 16 + 1023) / 1024 * 1024;
+  static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 48 + 1023) / 1024 * 1024;
   static constexpr uint32_t SMEM = RING_BYTES + kStagingBytes + BAR_BYTES + 1024;
   // A: K-major, one swizzle atom along K (BK*2 bytes = 32/64/128 B)
   static constexpr uint32_t A_LAYOUT = BK == 64 ? 2u : (BK == 32 ? 4u : 6u);
@@ -248,7 +302,8 @@ struct Cfg {
   static constexpr uint32_t B_LAYOUT = 2u;
   static constexpr uint32_t B_LBO = BK * 128;  // next 64-wide N chunk
   static constexpr uint32_t B_SBO = 1024;      // next 8 K-rows
-  static_assert(BN % 64 == 0 && BN <= 256, "BN");
+  static_assert(BN % 64 == 0 && BN <= 256 && BNC % 64 == 0, "BN");
+  static_assert(CG == 1 || CG == 2, "CG");
   static_assert(BK == 16 || BK == 32 || BK == 64, "BK");
   static_assert(STAGES >= 2, "stages");
   static_assert(SMEM <= 232448, "shared memory");
@@ -347,12 +402,23 @@ __device__ __forceinline__ void store_vec4(const GemmParams& p, uint64_t row, ui
   }
 }
 
-template <int BN, int BK>
+// Hand an accumulator stage back to the MMA issuer (the rank-0 CTA's barrier).
+template <int CG>
+__device__ __forceinline__ void release_acc_t(uint64_t* bar) {
+  if constexpr (CG == 1)
+    mbar_arrive(bar);
+  else
+    mbar_arrive_rank(bar, 0);
+}
+#define release_acc(bar) release_acc_t<CG>(bar)
+
+template <int BN, int BK, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     streamk_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
-  using C = Cfg<BN, BK>;
+  using C = Cfg<BN, BK, CG>;
+  constexpr uint32_t TILE_M = kBM * CG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -365,10 +431,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* red_bar = tempty_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_bar + 1);
+  uint64_t* split_smem = red_bar + 2;                       // phase-2 work list (2 tiles)
+  uint32_t* nsplit_smem = reinterpret_cast<uint32_t*>(red_bar + 4);
 
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
-  const uint32_t x = blockIdx.x;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // row half of the pair tile
+  const uint32_t x = blockIdx.x / CG;                      // workgroup (pair) id
   const Sched& s = p.s;
 
   if (warp == 0 && lane == 0) {
@@ -380,21 +449,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 4);
+      mbar_init(&tempty_bar[i], 4 * CG);  // every epilogue warp of the pair
     }
     mbar_init(red_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_shared();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    cluster_sync();  // peer barriers initialised and TMEM allocated on both CTAs
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) SKPP_STAMP(p, TL_START);
@@ -408,21 +489,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       cursor_init(cur, s, x);
       Item it;
       while (cursor_next(cur, s, x, it)) {
-        const int32_t m0 = (int32_t)(it.tile / s.n_tiles) * kBM;
-        const int32_t n0 = (int32_t)(it.tile % s.n_tiles) * BN;
+        const int32_t m0 = (int32_t)((it.tile / s.n_tiles) * TILE_M + rank * kBM);
+        const int32_t n0 = (int32_t)((it.tile % s.n_tiles) * BN + rank * C::BNC);
         for (uint64_t kk = it.kb; kk < it.ke; ++kk) {
           mbar_wait(&empty_bar[stage], phase ^ 1, 1);
-          mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          // the MMA-issuing (rank-0) CTA's barrier expects the bytes of the whole pair
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
           if (first_load) {
             SKPP_STAMP(p, TL_FIRST_TMA);
             first_load = false;
           }
           const int32_t k0 = (int32_t)(kk * BK);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
+          if constexpr (CG == 1) {
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j)
-            tma_load_2d(sB + stage * C::B_BYTES + j * (BK * 128), &tmB, n0 + 64 * j, k0,
-                        &full_bar[stage]);
+            for (int j = 0; j < C::BNC / 64; ++j)
+              tma_load_2d(sB + stage * C::B_BYTES + j * (BK * 128), &tmB, n0 + 64 * j, k0,
+                          &full_bar[stage]);
+          } else {
+            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
+#pragma unroll
+            for (int j = 0; j < C::BNC / 64; ++j)
+              tma_load_2d_pair(sB + stage * C::B_BYTES + j * (BK * 128), &tmB, n0 + 64 * j, k0,
+                               &full_bar[stage]);
+          }
           if (p.l2_prefetch) {
             // warm L2 with the k-blocks beyond the ring: up to p.l2_prefetch of them
             const uint64_t far = kk + C::STAGES + p.l2_prefetch - 1;
@@ -431,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int32_t kq0 = (int32_t)(kq * BK);
               tma_prefetch_2d(&tmA, kq0, m0);
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_prefetch_2d(&tmB, n0 + 64 * j, kq0);
+              for (int j = 0; j < C::BNC / 64; ++j) tma_prefetch_2d(&tmB, n0 + 64 * j, kq0);
             }
           }
           if (++stage == C::STAGES) {
@@ -442,8 +532,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (1 lane)
-    if (lane == 0) {
+    // ------------------------------------------------ MMA issuer (1 lane of the rank-0 CTA)
+    if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, local = 0;
       Cursor cur;
       cursor_init(cur, s, x);
@@ -463,15 +553,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = umma_desc(a_addr + k * 32, 0, C::A_SBO, C::A_LAYOUT);
             const uint64_t bd = umma_desc(b_addr + k * 2048, C::B_LBO, C::B_SBO, C::B_LAYOUT);
-            umma_f16(dtm, ad, bd, p.idesc, (kk > it.kb || k > 0) ? 1u : 0u);
+            if constexpr (CG == 1)
+              umma_f16(dtm, ad, bd, p.idesc, (kk > it.kb || k > 0) ? 1u : 0u);
+            else
+              umma_f16_pair(dtm, ad, bd, p.idesc, (kk > it.kb || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          if constexpr (CG == 1)
+            umma_commit(&empty_bar[stage]);
+          else
+            umma_commit_pair(&empty_bar[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[as]);
+        if constexpr (CG == 1)
+          umma_commit(&tfull_bar[as]);
+        else
+          umma_commit_pair(&tfull_bar[as]);
         ++local;
       }
       SKPP_STAMP(p, TL_MMA_DONE);
@@ -482,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = ew * 32 + lane;      // tile row held by this thread
     const uint32_t et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
     const bool leader = (et == 0);
+    const uint32_t cta = blockIdx.x;  // workspace slots are per CTA (per row half)
     const bool out16 = p.out_dtype != SKPP_F32;
     const uint32_t epoch = s.sk_tiles ? (ld_relaxed_gpu(p.hdr) + 1u) : 0u;
     const uint32_t stg_base = smem_u32(stg) + ew * 2 * kStageBuf;
@@ -493,14 +593,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     Item it;
     while (cursor_next(cur, s, x, it)) {
       const uint32_t as = local & 1, aph = (local >> 1) & 1;
-      if (leader) record_item(p, x, local, it);
+      if (leader && rank == 0) record_item(p, x, local, it);
       mbar_wait(&tfull_bar[as], aph, 4);
       tc_fence_after();
       if (leader && local == 0) SKPP_STAMP(p, TL_EPI_FIRST);
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + as * BN;
       const bool partial = it.role != ROLE_FULL;
-      const uint64_t slot = 2ull * x + (sk_seen == 0 ? 0 : 1);
-      const uint64_t tile_row0 = (it.tile / s.n_tiles) * kBM;
+      const uint64_t slot = 2ull * cta + (sk_seen == 0 ? 0 : 1);
+      const uint64_t tile_row0 = (it.tile / s.n_tiles) * TILE_M + rank * kBM;
       const uint64_t tile_col0 = (it.tile % s.n_tiles) * BN;
       if (partial) {
         // Partial slot layout: float4[BN/4][BM] ("column-group major"): a warp's
@@ -515,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c == BN / 32 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[as]);
+            if (lane == 0) release_acc(&tempty_bar[as]);
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -556,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // all TMEM reads of this item complete: hand the accumulator stage back
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[as]);
+            if (lane == 0) release_acc(&tempty_bar[as]);
           }
           if (p.c_tma) {
             const uint32_t buf = stg_base + sbuf * kStageBuf;
@@ -583,21 +683,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it.phase == PHASE_SK) ++sk_seen;
       ++local;
     }
-    if (leader && p.trace_counts != nullptr) p.trace_counts[x] = (int64_t)local;
+    if (leader && rank == 0 && p.trace_counts != nullptr) p.trace_counts[x] = (int64_t)local;
     if (leader) SKPP_STAMP(p, TL_PHASE1);
 
-    // ---- phase 2: cooperative fixed-order reduction of the split tiles.
-    // Contributor idx of a tile with nc contributors reduces column groups
-    // [idx*V/nc, (idx+1)*V/nc) over all nc slots, in increasing CTA order.
-    // The slices are pulled into the operand ring (idle now: every MMA of this
-    // CTA has completed) with bulk copies; each thread owns one tile row.
-    constexpr uint32_t V = BN / 4;       // float4 column groups per tile row
-    constexpr uint32_t GB = kBM * 16;    // bytes of one column group (all rows)
-    constexpr uint32_t NG = 8;           // column groups per pass (register accumulators)
-    uint32_t red_phase = 0;
-    const float4* ring = reinterpret_cast<const float4*>(smem);
+    // hand the split tiles to the whole CTA for phase 2
+    if (leader) {
+      split_smem[0] = split_tiles[0];
+      split_smem[1] = split_tiles[1];
+      nsplit_smem[0] = n_split;
+    }
+    if (lane == 0) bulk_wait<0>();  // staging must outlive the in-flight TMA stores
+  }
+
+  // ---- phase 2 (all 8 warps): cooperative fixed-order reduction of the split
+  // tiles.  Contributor idx of a tile with nc contributors reduces column
+  // groups [idx*V/nc, (idx+1)*V/nc) of its row half over all nc slots, in
+  // increasing CTA order.  Thread ft owns row (ft & 127) and, per pass of four
+  // column groups, groups jb + (ft >> 7) and jb + (ft >> 7) + 2.  Loads are
+  // coalesced (a warp reads 32 consecutive rows of one group = 512 B) and kept
+  // 16 deep per thread (64 KiB per CTA) because this step is bound by L2
+  // latency x bytes in flight, not by bandwidth.
+  __syncwarp();          // producer / MMA lanes rejoin their warps
+  phase2_bar_sync();     // split tiles published by the epilogue
+  if (s.sk_tiles) {
+    const uint32_t ft = threadIdx.x;
+    const uint32_t r = ft & 127, h = ft >> 7;
+    const uint32_t n_split = nsplit_smem[0];
+    const uint32_t epoch = ld_relaxed_gpu(p.hdr) + 1u;
+    constexpr uint32_t V = BN / 4;  // float4 column groups per tile row
+    const float4* wsv = reinterpret_cast<const float4*>(p.ws);
+    const uint64_t slot_v = (uint64_t)kBM * V;  // float4 per slot
     for (uint32_t si = 0; si < n_split; ++si) {
-      const uint64_t u = split_tiles[si];
+      const uint64_t u = split_smem[si];
       const uint64_t x0 = (u * s.ipt) / s.ipw;
       const uint64_t x1 = ((u + 1) * s.ipt - 1) / s.ipw;
       const uint32_t nc = (uint32_t)(x1 - x0 + 1);
@@ -605,11 +722,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t j0 = (uint32_t)(((uint64_t)idx * V) / nc);
       const uint32_t j1 = (uint32_t)(((uint64_t)(idx + 1) * V) / nc);
       if (j0 == j1) continue;
-      // contributor x0+t wrote its first Stream-K item (slot 2(x0+t)), except
-      // x0 when its range starts inside an earlier tile (tile u is its last item)
-      const uint64_t slot0 = 2 * x0 + ((x0 * s.ipw == u * s.ipt) ? 0 : 1);
-      for (uint32_t t = et; t < nc; t += 128) {
-        const uint64_t sl = t == 0 ? slot0 : 2 * (x0 + t);
+      // contributor x0+t wrote its first Stream-K item (slot 2*cta), except x0
+      // when its range starts inside an earlier tile (tile u is its last item)
+      const uint64_t slot0 = 2 * (x0 * CG + rank) + ((x0 * s.ipw == u * s.ipt) ? 0 : 1);
+      for (uint32_t t = ft; t < nc; t += kThreads) {
+        const uint64_t sl = t == 0 ? slot0 : 2 * ((x0 + t) * CG + rank);
         if (ld_acquire_gpu(p.flags + sl) != epoch) {
           const long long t0 = clock64();
           while (ld_acquire_gpu(p.flags + sl) != epoch) {
@@ -618,58 +735,76 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      epi_bar_sync();
-      if (leader && si == 0) SKPP_STAMP(p, TL_WAITED);
+      phase2_bar_sync();
+      if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
       const uint64_t tile = s.dp_tiles + u;
-      const uint64_t grow = (tile / s.n_tiles) * kBM + et;
+      const uint64_t grow = (tile / s.n_tiles) * TILE_M + rank * kBM + r;
       const uint64_t gcol0 = (tile % s.n_tiles) * BN;
-      for (uint32_t jb = j0; jb < j1; jb += NG) {
-        const uint32_t ng = (j1 - jb < NG) ? (j1 - jb) : NG;
-        const uint32_t bytes = ng * GB;
-        uint32_t tb = C::RING_BYTES / bytes;  // contributors per batch (>= 12)
-        if (tb > nc) tb = nc;
-        float4 acc[NG];
+      for (uint32_t jb = j0; jb < j1; jb += 4) {
+        const uint32_t ga = jb + h, gb = jb + h + 2;
+        if (ga >= j1) continue;
+        const bool two = gb < j1;
+        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+        const float4* base_a = wsv + (uint64_t)ga * kBM + r;
+        if (two) {
+          constexpr uint32_t KB = 8;
+          for (uint32_t t0 = 0; t0 < nc; t0 += KB) {
+            float4 q0[KB], q1[KB];
 #pragma unroll
-        for (uint32_t i = 0; i < NG; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint32_t t0 = 0; t0 < nc; t0 += tb) {
-          const uint32_t nb = (nc - t0 < tb) ? (nc - t0) : tb;
-          if (leader) {
-            fence_async_global();
-            mbar_arrive_expect_tx(red_bar, nb * bytes);
-            for (uint32_t t = 0; t < nb; ++t) {
-              const uint64_t sl = (t0 + t) == 0 ? slot0 : 2 * (x0 + t0 + t);
-              bulk_g2s(smem + t * bytes, p.ws + sl * (uint64_t)(kBM * BN) + (uint64_t)jb * kBM * 4,
-                       bytes, red_bar);
+            for (uint32_t b = 0; b < KB; ++b) {
+              if (t0 + b < nc) {
+                const uint64_t sl = (t0 + b) == 0 ? slot0 : 2 * ((x0 + t0 + b) * CG + rank);
+                q0[b] = ld_cg_f4(base_a + sl * slot_v);
+                q1[b] = ld_cg_f4(base_a + sl * slot_v + 2 * kBM);
+              }
             }
-          }
-          mbar_wait(red_bar, red_phase, 6);
-          red_phase ^= 1;
-          for (uint32_t t = 0; t < nb; ++t) {
 #pragma unroll
-            for (uint32_t i = 0; i < NG; ++i) {
-              if (i < ng) {
-                const float4 q = ring[(t * ng + i) * kBM + et];
-                acc[i].x += q.x;
-                acc[i].y += q.y;
-                acc[i].z += q.z;
-                acc[i].w += q.w;
+            for (uint32_t b = 0; b < KB; ++b) {
+              if (t0 + b < nc) {
+                acc0.x += q0[b].x;
+                acc0.y += q0[b].y;
+                acc0.z += q0[b].z;
+                acc0.w += q0[b].w;
+                acc1.x += q1[b].x;
+                acc1.y += q1[b].y;
+                acc1.z += q1[b].z;
+                acc1.w += q1[b].w;
               }
             }
           }
-          epi_bar_sync();  // the ring is overwritten by the next batch's copies
-        }
+        } else {
+          constexpr uint32_t KB = 16;
+          for (uint32_t t0 = 0; t0 < nc; t0 += KB) {
+            float4 q0[KB];
 #pragma unroll
-        for (uint32_t i = 0; i < NG; ++i)
-          if (i < ng) store_vec4(p, grow, gcol0 + 4 * (jb + i), acc[i]);
+            for (uint32_t b = 0; b < KB; ++b) {
+              if (t0 + b < nc) {
+                const uint64_t sl = (t0 + b) == 0 ? slot0 : 2 * ((x0 + t0 + b) * CG + rank);
+                q0[b] = ld_cg_f4(base_a + sl * slot_v);
+              }
+            }
+#pragma unroll
+            for (uint32_t b = 0; b < KB; ++b) {
+              if (t0 + b < nc) {
+                acc0.x += q0[b].x;
+                acc0.y += q0[b].y;
+                acc0.z += q0[b].z;
+                acc0.w += q0[b].w;
+              }
+            }
+          }
+        }
+        store_vec4(p, grow, gcol0 + 4 * ga, acc0);
+        if (two) store_vec4(p, grow, gcol0 + 4 * gb, acc1);
       }
     }
-    if (leader) SKPP_STAMP(p, TL_PHASE2);
-    if (lane == 0) bulk_wait<0>();  // staging must outlive the in-flight TMA stores
+    if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
     // ---- launch epilogue: the last CTA out advances the workspace epoch
-    if (s.sk_tiles && leader) {
+    phase2_bar_sync();
+    if (ft == 0) {
       __threadfence();
       const uint32_t done = atomicAdd(p.hdr + 1, 1u);
-      if (done == s.g - 1) {
+      if (done == gridDim.x - 1) {
         p.hdr[1] = 0u;
         __threadfence();
         p.hdr[0] = epoch;
@@ -678,12 +813,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    cluster_sync();  // the peer's MMAs into this CTA's TMEM are complete on both sides
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(C::TMEM_COLS)
-                 : "memory");
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -774,6 +918,7 @@ struct Plan {
   const void* func;
   uint32_t smem;
   uint32_t block_n;
+  uint32_t cg;      // CTAs per workgroup (2 = cta_group::2 pair)
   CUtensorMap ma, mb, mc;
   GemmParams p;
   skpp_sched_t cs;
@@ -781,72 +926,105 @@ struct Plan {
   void* ws_bound;   // workspace the parameters point into
 };
 
-template <int BN, int BK>
+template <int BN, int BK, int CG>
 static int kernel_setup(const void** func, uint32_t* smem) {
-  using C = Cfg<BN, BK>;
+  using C = Cfg<BN, BK, CG>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK>,
+    err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK, CG>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (err == cudaSuccess && CG == 2)
+      err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK, CG>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   });
   if (err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
     return SKPP_ELAUNCH;
   }
-  *func = reinterpret_cast<const void*>(streamk_gemm_kernel<BN, BK>);
+  *func = reinterpret_cast<const void*>(streamk_gemm_kernel<BN, BK, CG>);
   *smem = C::SMEM;
   return SKPP_OK;
 }
 
-template <int BN, int BK>
-static int max_coresident_impl(int* ctas) {
+// Co-resident workgroups (CTAs, or CTA pairs when CG == 2) of one launch.
+template <int BN, int BK, int CG>
+static int max_coresident_impl(int* groups) {
   constexpr int kMaxDev = 64;
   static int cache[kMaxDev] = {0};  // 0 = not yet queried
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur >= 0 && cur < kMaxDev && cache[cur] > 0) {
-    *ctas = cache[cur];
+    *groups = cache[cur];
     return SKPP_OK;
   }
   const void* func;
   uint32_t smem;
-  int rc = kernel_setup<BN, BK>(&func, &smem);
+  int rc = kernel_setup<BN, BK, CG>(&func, &smem);
   if (rc) return rc;
-  int per_sm = 0, sms = 0;
+  int sms = 0, n = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur);
-  cudaError_t e =
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, streamk_gemm_kernel<BN, BK>, kThreads, smem);
+  cudaError_t e;
+  if constexpr (CG == 1) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, streamk_gemm_kernel<BN, BK, CG>, kThreads, smem);
+    n *= sms;
+  } else {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(sms);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaOccupancyMaxActiveClusters(&n, streamk_gemm_kernel<BN, BK, CG>, &cfg);
+  }
   if (e != cudaSuccess) {
     set_error(std::string("occupancy query: ") + cudaGetErrorString(e));
     return SKPP_ELAUNCH;
   }
-  *ctas = per_sm * sms;
-  if (cur >= 0 && cur < kMaxDev) cache[cur] = *ctas;
+  *groups = n;
+  if (cur >= 0 && cur < kMaxDev) cache[cur] = n;
   return SKPP_OK;
 }
 
-// Calls f(integral_constant<BN>, integral_constant<BK>) for the instantiated tile shapes.
+// Calls f(integral_constant<BN>, integral_constant<BK>, integral_constant<CG>)
+// for the instantiated tile shapes: blk_m = 128 (one CTA) or 256 (CTA pair).
 template <typename F>
 static int dispatch_tile(const skpp_tile_t* t, F&& f) {
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
   using I16 = std::integral_constant<int, 16>;
   using I32 = std::integral_constant<int, 32>;
   using I64 = std::integral_constant<int, 64>;
   using I128 = std::integral_constant<int, 128>;
   using I256 = std::integral_constant<int, 256>;
-  if (t->blk_m != (uint32_t)kBM) return SKPP_ETILE;
-  if (t->blk_k == 64) {
-    if (t->blk_n == 64) return f(I64{}, I64{});
-    if (t->blk_n == 128) return f(I128{}, I64{});
-    if (t->blk_n == 256) return f(I256{}, I64{});
-  } else if (t->blk_k == 32) {
-    if (t->blk_n == 64) return f(I64{}, I32{});
-    if (t->blk_n == 128) return f(I128{}, I32{});
-    if (t->blk_n == 256) return f(I256{}, I32{});
-  } else if (t->blk_k == 16) {
-    if (t->blk_n == 64) return f(I64{}, I16{});
-    if (t->blk_n == 128) return f(I128{}, I16{});
-    if (t->blk_n == 256) return f(I256{}, I16{});
+  if (t->blk_m == (uint32_t)kBM) {
+    if (t->blk_k == 64) {
+      if (t->blk_n == 64) return f(I64{}, I64{}, I1{});
+      if (t->blk_n == 128) return f(I128{}, I64{}, I1{});
+      if (t->blk_n == 256) return f(I256{}, I64{}, I1{});
+    } else if (t->blk_k == 32) {
+      if (t->blk_n == 64) return f(I64{}, I32{}, I1{});
+      if (t->blk_n == 128) return f(I128{}, I32{}, I1{});
+      if (t->blk_n == 256) return f(I256{}, I32{}, I1{});
+    } else if (t->blk_k == 16) {
+      if (t->blk_n == 64) return f(I64{}, I16{}, I1{});
+      if (t->blk_n == 128) return f(I128{}, I16{}, I1{});
+      if (t->blk_n == 256) return f(I256{}, I16{}, I1{});
+    }
+  } else if (t->blk_m == 2u * kBM) {
+    if (t->blk_k == 64) {
+      if (t->blk_n == 128) return f(I128{}, I64{}, I2{});
+      if (t->blk_n == 256) return f(I256{}, I64{}, I2{});
+    } else if (t->blk_k == 32) {
+      if (t->blk_n == 128) return f(I128{}, I32{}, I2{});
+      if (t->blk_n == 256) return f(I256{}, I32{}, I2{});
+    }
   }
   return SKPP_ETILE;
 }
@@ -878,17 +1056,16 @@ using namespace skpp;
 
 extern "C" int skpp_tile_supported(const skpp_tile_t* t) {
   if (!t) return 0;
-  if (t->blk_m != (uint32_t)kBM) return 0;
-  if (t->blk_n != 64 && t->blk_n != 128 && t->blk_n != 256) return 0;
-  if (t->blk_k != 16 && t->blk_k != 32 && t->blk_k != 64) return 0;
-  return 1;
+  return dispatch_tile(t, [](auto, auto, auto) { return SKPP_OK; }) == SKPP_OK ? 1 : 0;
 }
 
 extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_tile_t* t,
                                          uint32_t g) {
   (void)p;
   if (!t) return 0;
-  return kWsHeader + ws_flag_bytes(g) + 2ull * g * t->blk_m * t->blk_n * 4;
+  // two partial slots (first / last Stream-K item) of 128 x blk_n fp32 per CTA
+  const uint64_t ctas = (uint64_t)g * (t->blk_m > (uint32_t)kBM ? 2 : 1);
+  return kWsHeader + ws_flag_bytes(ctas) + 2ull * ctas * kBM * t->blk_n * 4;
 }
 
 extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
@@ -919,9 +1096,9 @@ extern "C" int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major
   return SKPP_OK;
 }
 
-static int max_coresident_dispatch(const skpp_tile_t* t, int* ctas) {
-  return dispatch_tile(t, [&](auto bn, auto bk) {
-    return max_coresident_impl<decltype(bn)::value, decltype(bk)::value>(ctas);
+static int max_coresident_dispatch(const skpp_tile_t* t, int* groups) {
+  return dispatch_tile(t, [&](auto bn, auto bk, auto cg) {
+    return max_coresident_impl<decltype(bn)::value, decltype(bk)::value, decltype(cg)::value>(groups);
   });
 }
 
@@ -1003,14 +1180,15 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
       return SKPP_EGRID;
     }
   }
-  rc = dispatch_tile(t, [&](auto bn, auto bk) {
-    return kernel_setup<decltype(bn)::value, decltype(bk)::value>(&pl->func, &pl->smem);
+  rc = dispatch_tile(t, [&](auto bn, auto bk, auto cg) {
+    return kernel_setup<decltype(bn)::value, decltype(bk)::value, decltype(cg)::value>(&pl->func, &pl->smem);
   });
   if (rc) {
     delete pl;
     return rc;
   }
   pl->block_n = t->blk_n;
+  pl->cg = t->blk_m / kBM;
   const uint32_t BK = t->blk_k;
   const CUtensorMapSwizzle aswz = BK == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : BK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
@@ -1030,7 +1208,7 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   gp.N = (uint32_t)p->n;
   const uint32_t ab = ops->in_dtype == SKPP_BF16 ? 1u : 0u;
   gp.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (0u << 15) | (1u << 16) |
-             ((uint32_t)(t->blk_n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+             ((uint32_t)(t->blk_n >> 3) << 17) | ((uint32_t)(t->blk_m >> 4) << 24);
   gp.out_dtype = ops->out_dtype;
   gp.C = ops->c;
   gp.ldc = (uint64_t)ops->ldc;
@@ -1076,7 +1254,7 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
       uint8_t* base = reinterpret_cast<uint8_t*>(workspace);
       gp.hdr = reinterpret_cast<uint32_t*>(base);
       gp.flags = reinterpret_cast<uint32_t*>(base + kWsHeader);
-      gp.ws = reinterpret_cast<float*>(base + kWsHeader + ws_flag_bytes(pl->cs.g));
+      gp.ws = reinterpret_cast<float*>(base + kWsHeader + ws_flag_bytes((uint64_t)pl->cs.g * pl->cg));
       pl->ws_bound = workspace;
     }
   }
@@ -1085,21 +1263,28 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(pl->cs.g);
+  cfg.gridDim = dim3(pl->cs.g * pl->cg);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = pl->smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
   cfg.numAttrs = 0;
-  if (pl->cs.sk_tiles > 0) {
+  if (pl->cg == 2) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attr[cfg.numAttrs].val.clusterDim.x = 2;
+    attr[cfg.numAttrs].val.clusterDim.y = 1;
+    attr[cfg.numAttrs].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
+  } else if (pl->cs.sk_tiles > 0) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cap);
     if (cap == cudaStreamCaptureStatusNone) {
       // Stream-K contributors wait on each other: every CTA must be resident at once.
-      attr[0].id = cudaLaunchAttributeCooperative;
-      attr[0].val.cooperative = 1;
-      cfg.numAttrs = 1;
+      // (Cluster launches rely on the host-side co-residency check instead.)
+      attr[cfg.numAttrs].id = cudaLaunchAttributeCooperative;
+      attr[cfg.numAttrs].val.cooperative = 1;
+      ++cfg.numAttrs;
     }
   }
   void* args[4] = {&pl->ma, &pl->mb, &pl->mc, &gp};

@@ -126,6 +126,12 @@ def max_coresident(tile: TileShape) -> int:
     return int(n.value)
 
 
+def default_g(tile: TileShape, device: int | None = None) -> int:
+    """Persistent workgroups of one launch: one CTA per SM, or one CTA pair per
+    two SMs for 256-row (cta_group::2) tiles."""
+    return sm_count(device) // (2 if tile.blk_m == 256 else 1)
+
+
 def tile_supported(tile: TileShape) -> bool:
     return bool(_lib.lib.skpp_tile_supported(_lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k)))
 
@@ -186,14 +192,15 @@ class GemmPlan:
         if not tile_supported(tile):
             raise ValueError(
                 f"tile {tile.blk_m}x{tile.blk_n}x{tile.blk_k} is not implemented by the sm_100a "
-                "kernel (blk_m=128, blk_n in {64,128,256}, blk_k in {16,32,64})"
+                "kernel (blk_m=128: blk_n in {64,128,256}, blk_k in {16,32,64}; "
+                "blk_m=256 CTA pair: blk_n in {128,256}, blk_k in {32,64})"
             )
         m, k = a.shape
         n = b.shape[1]
         self.size = ProblemSize(int(m), int(n), int(k))
         self.tile = tile
         self.policy = policy
-        self.g = sm_count(dev) if g is None else int(g)
+        self.g = default_g(tile, dev) if g is None else int(g)
         self.a, self.b, self.c = a, b, c  # keep the operands alive as long as the plan
         self.device = dev
         self.sched_c = closed_form(self.size, tile, self.g, policy)

@@ -32,7 +32,7 @@ from dataclasses import dataclass
 import torch
 
 from .costmodel import CostEstimate, TuneRecord, rank_costs
-from .executor import GemmPlan, sm_count
+from .executor import GemmPlan, default_g
 from .scheduler import count_partials, schedule_signature
 from .types import Policy, ProblemSize, TileShape, canonical_policies
 
@@ -166,7 +166,7 @@ def tune_sizes(
     if params is None:
         params = MeasureParams()
     if g is None:
-        g = sm_count()
+        g = default_g(tile)
     if pool is None:
         pool = OperandPool(sizes, params.in_dtype, params.out_dtype)
     out = []

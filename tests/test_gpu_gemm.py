@@ -63,10 +63,29 @@ def _policies():
     ],
 )
 def test_integer_inputs_bitwise_every_policy(m, n, k, blk_n, blk_k):
+    _bitwise_every_policy(m, n, k, 128, blk_n, blk_k)
+
+
+@pytest.mark.parametrize(
+    "m,n,k,blk_n,blk_k",
+    [
+        (256, 256, 256, 256, 64),     # one pair tile
+        (1024, 1024, 1024, 256, 64),
+        (512, 512, 8192, 128, 64),    # fixup-heavy
+        (600, 392, 1000, 256, 64),    # ragged: half-empty second CTA rows / columns
+        (300, 200, 520, 128, 32),
+    ],
+)
+def test_cta_pair_tiles_bitwise_every_policy(m, n, k, blk_n, blk_k):
+    """cta_group::2 tiles (256 rows over a CTA pair, g = SMs/2 workgroups)."""
+    _bitwise_every_policy(m, n, k, 256, blk_n, blk_k)
+
+
+def _bitwise_every_policy(m, n, k, blk_m, blk_n, blk_k):
     sk = _sk()
     a, b = _int_case(m, n, k, seed=m + n + k)
     want = ogemm.reference_gemm(a, b)
-    tile = sk.TileShape(128, blk_n, blk_k)
+    tile = sk.TileShape(blk_m, blk_n, blk_k)
     for pol in _policies():
         got, _ = _run(a, b, pol, tile)
         g = got.double().cpu().numpy()
@@ -96,15 +115,31 @@ def test_device_trace_matches_closed_form_and_oracle():
         assert got == want, pol.label
 
 
+def test_cta_pair_trace_matches_oracle():
+    sk = _sk()
+    size = sk.ProblemSize(1024, 2048, 2048)
+    a, b = _int_case(size.m, size.n, size.k, seed=3)
+    want = ogemm.reference_gemm(a, b)
+    for pol in _policies():
+        got, plan = _run(a, b, pol, sk.TileShape(256, 256, 64), trace_cap=64)
+        assert plan.g == 74
+        assert np.array_equal(got.double().cpu().numpy(), want), pol.label
+        dev = [[row[:5] for row in wg] for wg in plan.trace_items()]
+        ref = osched.build_schedule(size.m, size.n, size.k, 256, 256, 64, 74, pol.kind.value, pol.sk_batches, pol.sk_first)
+        assert dev == ref, pol.label
+
+
 def test_fp16_and_output_dtypes():
     sk = _sk()
     a, b = _int_case(512, 256, 1024, seed=7)
     want = ogemm.reference_gemm(a, b)
-    for in_dt in (torch.float16, torch.bfloat16):
-        for out_dt in (torch.float32, torch.bfloat16, torch.float16):
-            got, _ = _run(a, b, sk.Policy.all_stream_k(), sk.TileShape(128, 128, 64), in_dtype=in_dt, out_dtype=out_dt)
-            ref = torch.from_numpy(want).to(out_dt).double().numpy()
-            assert np.array_equal(got.double().cpu().numpy(), ref), (in_dt, out_dt)
+    for tile in (sk.TileShape(128, 128, 64), sk.TileShape(256, 256, 64)):
+        for in_dt in (torch.float16, torch.bfloat16):
+            for out_dt in (torch.float32, torch.bfloat16, torch.float16):
+                for pol in (sk.Policy.data_parallel(), sk.Policy.all_stream_k()):
+                    got, _ = _run(a, b, pol, tile, in_dtype=in_dt, out_dtype=out_dt)
+                    ref = torch.from_numpy(want).to(out_dt).double().numpy()
+                    assert np.array_equal(got.double().cpu().numpy(), ref), (tile, in_dt, out_dt, pol.label)
 
 
 def test_randn_within_tolerance_and_deterministic():

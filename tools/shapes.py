@@ -38,9 +38,9 @@ def main() -> None:
     sizes = [sk.ProblemSize(*s) for s in shapes]
     pool = sweep.OperandPool(sizes, dt, torch.float32)
     params = sweep.MeasureParams(warmup=3, reps=10, in_dtype=dt)
-    g = sk.executor.sm_count()
     for tile_s in args.tiles.split(","):
         tile = sk.TileShape(*(int(v) for v in tile_s.split("x")))
+        g = sk.executor.default_g(tile)
         for size in sizes:
             rec = sweep.measure_size(size, tile, g, sk.canonical_policies(), params, pool)
             out = {
