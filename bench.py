@@ -11,8 +11,9 @@ the Stream-K++ selection layer picks:
      winner, and the selected policy is the fastest measured candidate of
      ``bank.query(size) | {data-parallel}``;
   2. timed region: K steps, one persistent-kernel launch per step, L2
-     flushed (256 MiB write) before every step outside the per-step CUDA
-     events; device time is the sum of per-step event times, max over ranks.
+     flushed before every step (256 MiB write, then a 256 MiB read so the
+     resident lines are clean) outside the per-step CUDA events; device time
+     is the sum of per-step event times, max over ranks.
 
 Also reported: ``e2e`` (the same GEMM through the public
 ``execute_schedule`` with pinned host bf16 inputs, H2D + kernel + D2H every
@@ -139,6 +140,19 @@ def dist_setup(n_gpus: int):
     return world, rank, local
 
 
+def ncu_traffic(workload: str):
+    """DRAM bytes per launch of the GEMM kernel from the committed ncu capture of this workload
+    (profiles/ncu_bench_<workload>.json, made by tools/gpurun_profile.sh), or None."""
+    path = os.path.join(ROOT, "profiles", f"ncu_bench_{workload}.json")
+    try:
+        with open(path) as fh:
+            rows = json.load(fh)
+        row = next(r for r in rows if "streamk_gemm" in r.get("kernel", ""))
+        return int(row["dram_traffic_bytes"]), os.path.relpath(path, ROOT)
+    except (OSError, ValueError, KeyError, StopIteration):
+        return None, None
+
+
 def roofline(flops: float, nbytes: float, seconds: float, peaks: dict) -> dict:
     t_tc = flops / (peaks["bf16_tflops"] * 1e12)
     t_hbm = nbytes / (peaks["hbm_gbs"] * 1e9)
@@ -247,11 +261,21 @@ def run_ours(args, wl: dict) -> None:
     plan = sk.GemmPlan(a, b, c, policy, tile, g)
     flops = 2.0 * m * n * k
     nbytes = 2.0 * (m * k + k * n) + 4.0 * m * n
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+    # L2 flush between steps: write 256 MiB (> 126 MB L2), then read another 256 MiB so the
+    # lines left behind are clean (otherwise the GEMM pays the write-back of the flush's
+    # dirty lines).  Both run outside the per-step events.
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    scrub = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    sink = torch.empty(1, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        flush.zero_()
+        torch.sum(scrub, dim=0, out=sink)
+
     stream = torch.cuda.current_stream()
 
     for _ in range(max(args.warmup, 3)):
-        flush.zero_()
+        flush_l2()
         plan.launch()
     torch.cuda.synchronize()
 
@@ -262,7 +286,7 @@ def run_ours(args, wl: dict) -> None:
     torch.cuda.synchronize()
     with ClockSampler(physical_gpu(local)) as clocks:
         for i in range(args.steps):
-            flush.zero_()
+            flush_l2()
             starts[i].record(stream)
             plan.launch()
             ends[i].record(stream)
@@ -305,6 +329,12 @@ def run_ours(args, wl: dict) -> None:
                                     max_seconds=args.cpu_seconds, max_reps=20)
         cpu_value = flops / statistics.median(cpu_times) / 1e12
         per_policy = {p.label: round(size.flops / (e.makespan * 1e-6) / 1e12, 2) for p, e in rec.costs}
+        roof = roofline(flops, nbytes, per_step_s, peaks)
+        roof["algorithmic_bytes"] = int(nbytes)
+        roof["algorithmic_flops"] = int(flops)
+        traffic, tsrc = ncu_traffic(args.workload)
+        roof["traffic"] = traffic
+        roof["traffic_source"] = tsrc
         best_us = min(e.makespan for _, e in rec.costs)
         chosen_us = dict((p, e) for p, e in rec.costs)[policy].makespan
         line = {
@@ -323,7 +353,7 @@ def run_ours(args, wl: dict) -> None:
             "config": {
                 "workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]), "g": g,
                 "policy": policy.label, "out_dtype": "fp32",
-                "l2": "flushed before every step (256 MiB write outside the per-step events)",
+                "l2": "flushed before every step: 256 MiB write + 256 MiB read (clean lines), outside the per-step events",
                 "parallelism": f"replicas x{world} (GEMM is single-GPU)",
             },
             "pct_of_dense_peak": {
@@ -338,7 +368,7 @@ def run_ours(args, wl: dict) -> None:
                 "per_policy_tflops": per_policy,
                 "note": "per-policy times from CUDA-graph replays with warm L2 (selection sweep)",
             },
-            "roofline": roofline(flops, nbytes, per_step_s, peaks),
+            "roofline": roof,
             "cpu_baseline": {
                 "value": round(cpu_value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
                 "sample": f"{len(cpu_times)} full {m}x{n}x{k} runs of the oracle port of gemmsched "

@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t epoch = s.sk_tiles ? (ld_relaxed_gpu(p.hdr) + 1u) : 0u;
     const uint32_t stg_base = smem_u32(stg) + ew * 2 * kStageBuf;
     uint32_t sbuf = 0;  // staging buffer toggle of this warp
-    uint64_t split_tiles[2];
+    uint64_t split_tiles[1];
     uint32_t n_split = 0, sk_seen = 0, local = 0;
     Cursor cur;
     cursor_init(cur, s, x);
@@ -631,7 +631,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_release_gpu(p.flags + slot, epoch);
         }
         if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_FLAG);
-        split_tiles[n_split++] = it.tile - s.dp_tiles;
+        // the CTA reduces (phase 2) only the tile of its FIRST Stream-K item
+        if (sk_seen == 0) split_tiles[n_split++] = it.tile - s.dp_tiles;
       } else {
         // One chunk = 128 bytes of a row: 32 fp32 columns or 64 16-bit columns.
         const int ccols = out16 ? 64 : 32;
@@ -689,16 +690,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // hand the split tiles to the whole CTA for phase 2
     if (leader) {
       split_smem[0] = split_tiles[0];
-      split_smem[1] = split_tiles[1];
       nsplit_smem[0] = n_split;
     }
     if (lane == 0) bulk_wait<0>();  // staging must outlive the in-flight TMA stores
   }
 
   // ---- phase 2 (all 8 warps): cooperative fixed-order reduction of the split
-  // tiles.  Contributor idx of a tile with nc contributors reduces column
-  // groups [idx*V/nc, (idx+1)*V/nc) of its row half over all nc slots, in
-  // increasing CTA order.  Thread ft owns row (ft & 127) and, per pass of four
+  // tile of this CTA's first Stream-K item.  The reducers of tile u are the
+  // contributors whose first Stream-K item lies in u: x0 (only if its range
+  // starts exactly at the tile) .. x1, so every CTA reduces at most one tile
+  // and every split tile has at least one reducer (x1).  Reducer idx of nr
+  // sums column groups [idx*V/nr, (idx+1)*V/nr) of its row half over ALL nc
+  // contributors' slots, in increasing CTA order.  Thread ft owns row (ft & 127) and, per pass of four
   // column groups, groups jb + (ft >> 7) and jb + (ft >> 7) + 2.  Loads are
   // coalesced (a warp reads 32 consecutive rows of one group = 512 B) and kept
   // 16 deep per thread (64 KiB per CTA) because this step is bound by L2
@@ -718,13 +721,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t x0 = (u * s.ipt) / s.ipw;
       const uint64_t x1 = ((u + 1) * s.ipt - 1) / s.ipw;
       const uint32_t nc = (uint32_t)(x1 - x0 + 1);
-      const uint32_t idx = (uint32_t)(x - x0);
-      const uint32_t j0 = (uint32_t)(((uint64_t)idx * V) / nc);
-      const uint32_t j1 = (uint32_t)(((uint64_t)(idx + 1) * V) / nc);
+      const bool aligned = x0 * s.ipw == u * s.ipt;  // x0's range starts at tile u
+      const uint64_t r_lo = x0 + (aligned ? 0 : 1);
+      const uint32_t nr = (uint32_t)(x1 - r_lo + 1);
+      const uint32_t idx = (uint32_t)(x - r_lo);
+      const uint32_t j0 = (uint32_t)(((uint64_t)idx * V) / nr);
+      const uint32_t j1 = (uint32_t)(((uint64_t)(idx + 1) * V) / nr);
       if (j0 == j1) continue;
       // contributor x0+t wrote its first Stream-K item (slot 2*cta), except x0
       // when its range starts inside an earlier tile (tile u is its last item)
-      const uint64_t slot0 = 2 * (x0 * CG + rank) + ((x0 * s.ipw == u * s.ipt) ? 0 : 1);
+      const uint64_t slot0 = 2 * (x0 * CG + rank) + (aligned ? 0 : 1);
       for (uint32_t t = ft; t < nc; t += kThreads) {
         const uint64_t sl = t == 0 ? slot0 : 2 * ((x0 + t) * CG + rank);
         if (ld_acquire_gpu(p.flags + sl) != epoch) {

@@ -1,0 +1,199 @@
+"""GPU tests of the public drop-in API (execute_schedule / run_equivalence / gemm).
+
+Mirrors the reference's executor tests (tests/test_executor.py in gemmsched):
+every canonical policy bitwise-equal to the float64 oracle on integer inputs,
+ragged edges, shuffled-order and threaded arguments, error messages — plus the
+device-specific contracts: CUDA-graph replays, workspace reuse, unaligned
+operands, and that the native library is what actually runs.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import gemm as ogemm
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def sk():
+    import paper_2408_11417_b200 as m
+
+    return m
+
+
+def instance(size, tile, g, policy, seed=0):
+    rng = np.random.default_rng(seed)
+    a = ogemm.random_int_matrix(size.m, size.k, rng)
+    b = ogemm.random_int_matrix(size.k, size.n, rng)
+    sched = sk().build_schedule(size, tile, sk().HardwareModel(g, 1), policy)
+    return a, b, sched
+
+
+def test_native_library_is_loaded():
+    from paper_2408_11417_b200 import _lib
+
+    maps = open("/proc/self/maps").read()
+    assert str(_lib.LIB_PATH) in maps
+
+
+def test_every_canonical_policy_matches_reference_numpy_path():
+    m = sk()
+    size, tile = m.ProblemSize(384, 256, 640), m.TileShape(128, 128, 64)
+    for policy in m.canonical_policies():
+        a, b, sched = instance(size, tile, 148, policy, seed=11)
+        got = m.execute_schedule(a, b, sched, tile, size)
+        assert got.dtype == np.float64
+        assert np.array_equal(got, m.reference_gemm(a, b)), policy
+
+
+def test_ragged_unaligned_k_and_n_are_padded_transparently():
+    m = sk()
+    size, tile = m.ProblemSize(100, 75, 53), m.TileShape(128, 64, 16)
+    for policy in (m.Policy.data_parallel(), m.Policy.hybrid(3), m.Policy.all_stream_k()):
+        a, b, sched = instance(size, tile, 7, policy, seed=4)
+        got = m.execute_schedule(a, b, sched, tile, size)
+        assert np.array_equal(got, m.reference_gemm(a, b)), policy
+
+
+def test_shuffled_and_threaded_arguments_are_accepted_and_exact():
+    m = sk()
+    size, tile = m.ProblemSize(256, 256, 512), m.TileShape(128, 128, 64)
+    a, b, sched = instance(size, tile, 148, m.Policy.hybrid(2), seed=5)
+    base = m.execute_schedule(a, b, sched, tile, size)
+    for trial in range(3):
+        shuffled = m.execute_schedule(a, b, sched, tile, size, order="shuffled", rng=np.random.default_rng(trial))
+        assert shuffled.tobytes() == base.tobytes()
+    assert np.array_equal(m.execute_schedule(a, b, sched, tile, size, workers=4), base)
+
+
+def test_error_messages_match_reference():
+    m = sk()
+    size, tile = m.ProblemSize(128, 128, 64), m.TileShape(128, 128, 64)
+    a, b, sched = instance(size, tile, 148, m.Policy.data_parallel())
+    with pytest.raises(ValueError, match="rng"):
+        m.execute_schedule(a, b, sched, tile, size, order="shuffled")
+    with pytest.raises(ValueError, match="order"):
+        m.execute_schedule(a, b, sched, tile, size, order="sideways")
+    with pytest.raises(ValueError, match="do not match"):
+        m.execute_schedule(a[:8], b, sched, tile, size)
+    other = m.ProblemSize(128, 128, 128)
+    a2, b2, _ = instance(other, tile, 148, m.Policy.data_parallel())
+    with pytest.raises(ValueError, match="different problem"):
+        m.execute_schedule(a2, b2, sched, tile, other)
+    with pytest.raises(ValueError, match="inner dimensions"):
+        m.reference_gemm(np.zeros((2, 3)), np.zeros((4, 2)))
+    with pytest.raises(ValueError, match="not implemented"):
+        t2 = m.TileShape(64, 64, 32)
+        m.execute_schedule(a, b, m.build_schedule(size, t2, m.HardwareModel(148, 1), m.Policy.data_parallel()), t2, size)
+
+
+def test_hand_edited_schedule_is_rejected():
+    m = sk()
+    size, tile = m.ProblemSize(256, 256, 256), m.TileShape(128, 128, 64)
+    a, b, sched = instance(size, tile, 148, m.Policy.all_stream_k())
+    items = [list(wg) for wg in sched.assignments]
+    first = next(i for i, wg in enumerate(items) if wg)
+    del items[first][0]
+    bad = m.Schedule(sched.grid, sched.g, sched.policy, tuple(tuple(w) for w in items))
+    assert not m.validate_schedule(bad).covered_once
+    with pytest.raises(ValueError, match="closed form"):
+        m.execute_schedule(a, b, bad, tile, size)
+
+
+@pytest.mark.parametrize("policy_idx", range(7))
+def test_run_equivalence_like_reference(policy_idx):
+    m = sk()
+    policy = m.canonical_policies()[policy_idx]
+    for size in (m.ProblemSize(1, 64, 16), m.ProblemSize(100, 100, 100), m.ProblemSize(256, 256, 256)):
+        rep = m.run_equivalence(size, m.TileShape(128, 128, 64), m.HardwareModel(104, 1), policy, rng_seed=42)
+        assert rep.exact_match and rep.max_abs_diff == 0.0, (size, policy)
+
+
+def test_torch_cuda_and_host_tensors():
+    m = sk()
+    size, tile = m.ProblemSize(512, 384, 2048), m.TileShape(256, 256, 64)
+    a, b, sched = instance(size, tile, 74, m.Policy.hybrid(1), seed=9)
+    want = ogemm.reference_gemm(a, b)
+    at, bt = torch.from_numpy(a).to(torch.bfloat16), torch.from_numpy(b).to(torch.bfloat16)
+    dev = m.execute_schedule(at.cuda(), bt.cuda(), sched, tile, size)
+    assert dev.is_cuda and np.array_equal(dev.double().cpu().numpy(), want)
+    host = m.execute_schedule(at.pin_memory(), bt.pin_memory(), sched, tile, size)
+    assert not host.is_cuda and np.array_equal(host.double().numpy(), want)
+
+
+def test_unaligned_output_uses_direct_stores():
+    m = sk()
+    size = m.ProblemSize(256, 200, 512)
+    a, b, _ = instance(size, m.TileShape(128, 128, 64), 148, m.Policy.data_parallel(), seed=2)
+    at = torch.from_numpy(a).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(b).to(torch.bfloat16).cuda()
+    big = torch.zeros(256, 203, device="cuda")  # row stride 203 floats: not 16-byte aligned
+    c = big[:, 1:201]
+    for pol in (m.Policy.data_parallel(), m.Policy.all_stream_k()):
+        c.zero_()
+        m.GemmPlan(at, bt, c, pol, m.TileShape(128, 128, 64)).launch()
+        torch.cuda.synchronize()
+        assert np.array_equal(c.double().cpu().numpy(), ogemm.reference_gemm(a, b)), pol
+        assert float(big[:, 0].abs().sum()) == 0.0 and float(big[:, 201:].abs().sum()) == 0.0
+
+
+def test_cuda_graph_replays_and_workspace_reuse():
+    """Epoch-tagged flags keep graph replays (frozen parameters) correct."""
+    m = sk()
+    rng = np.random.default_rng(8)
+    shapes = [(512, 512, 4096), (384, 256, 2048)]
+    plans, wants = [], []
+    for mm, nn, kk in shapes:
+        a = ogemm.random_int_matrix(mm, kk, rng)
+        b = ogemm.random_int_matrix(kk, nn, rng)
+        at = torch.from_numpy(a).to(torch.bfloat16).cuda()
+        bt = torch.from_numpy(b).to(torch.bfloat16).cuda()
+        c = torch.zeros(mm, nn, device="cuda")
+        plans.append(m.GemmPlan(at, bt, c, m.Policy.all_stream_k(), m.TileShape(128, 128, 64)))
+        wants.append(ogemm.reference_gemm(a, b))
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        for p in plans:
+            p.launch()  # warm the per-stream workspace outside capture
+        side.synchronize()
+        with torch.cuda.graph(graph, stream=side):
+            for _ in range(3):
+                for p in plans:
+                    p.launch()
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(5):
+        for p in plans:
+            p.c.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        for p, want in zip(plans, wants):
+            assert np.array_equal(p.c.double().cpu().numpy(), want)
+
+
+def test_device_schedule_trace_kernel_matches_host():
+    m = sk()
+    from paper_2408_11417_b200 import _lib, scheduler
+
+    for size, tile, g, pol in [
+        (m.ProblemSize(8192, 14336, 4096), m.TileShape(128, 128, 64), 148, m.Policy.hybrid(3)),
+        (m.ProblemSize(1, 64, 65536), m.TileShape(128, 128, 64), 148, m.Policy.all_stream_k()),
+        (m.ProblemSize(4096, 4096, 4096), m.TileShape(256, 256, 64), 74, m.Policy.hybrid(2, False)),
+    ]:
+        sc = scheduler.closed_form(size, tile, g, pol)
+        items, offsets = scheduler.schedule_arrays(sc)
+        cap = int(max(offsets[x + 1] - offsets[x] for x in range(g)))
+        trace = torch.full((g, cap, 6), -1, dtype=torch.int64, device="cuda")
+        counts = torch.zeros(g, dtype=torch.int64, device="cuda")
+        _lib.check(_lib.lib.skpp_schedule_trace_device(
+            _lib.Problem(size.m, size.n, size.k), _lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k),
+            scheduler.policy_to_c(pol), g, trace.data_ptr(), cap, counts.data_ptr(),
+            torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        tr, cn = trace.cpu().numpy(), counts.cpu().numpy()
+        for x in range(g):
+            lo, hi = int(offsets[x]), int(offsets[x + 1])
+            assert cn[x] == hi - lo
+            assert np.array_equal(tr[x, : hi - lo], items[lo:hi])
