@@ -402,6 +402,91 @@ __device__ __forceinline__ void store_vec4(const GemmParams& p, uint64_t row, ui
   }
 }
 
+struct ReduceArgs {
+  const float4* wsv;   // workspace slots as float4[2g_cta][BN/4][128]
+  uint64_t slot_v;     // float4 per slot
+  uint64_t slot0;      // slot of contributor x0 (first or last item)
+  uint64_t x0;         // first contributing workgroup
+  uint32_t rank;       // row half (CTA rank in the pair)
+  uint32_t nc;         // contributors
+};
+
+__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t epoch) {
+  if (ld_acquire_gpu(flag) == epoch) return;
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(flag) != epoch) {
+    __nanosleep(32);
+    watchdog(t0, 5);
+  }
+}
+
+// Phase 2(a): part[(j - j0)*128 + r] = sum over peers t = 1..nc-1 (in order) of
+// slot(x0+t)[j][r] for this thread's column groups j = ga, ga+2, ... < j1.
+template <int G, int KB, int CG>
+__device__ __forceinline__ void sum_peers(const ReduceArgs& ra, const float4* base_r, uint32_t ga,
+                                          uint32_t j0, uint32_t j1, float4* part, uint32_t r) {
+  for (uint32_t jb = ga; jb < j1; jb += 2 * G) {
+    float4 acc[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t t0 = 1; t0 < ra.nc; t0 += KB) {
+      float4 q[G][KB];
+#pragma unroll
+      for (int b = 0; b < KB; ++b) {
+        if (t0 + b < ra.nc) {
+          const float4* src = base_r + 2 * ((ra.x0 + t0 + b) * CG + ra.rank) * ra.slot_v;
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            if (jb + 2 * g < j1) q[g][b] = ld_cg_f4(src + (uint64_t)(jb + 2 * g) * kBM);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < KB; ++b) {
+        if (t0 + b < ra.nc) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            if (jb + 2 * g < j1) {
+              acc[g].x += q[g][b].x;
+              acc[g].y += q[g][b].y;
+              acc[g].z += q[g][b].z;
+              acc[g].w += q[g][b].w;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (jb + 2 * g < j1) part[(jb + 2 * g - j0) * kBM + r] = acc[g];
+  }
+}
+
+// Phase 2(b): C[row][j] = part + slot(x0)[j][r], 8 loads of x0's slot in flight.
+__device__ __forceinline__ void add_owner_and_store(const GemmParams& p, const ReduceArgs& ra,
+                                                    const float4* base_r, uint32_t ga, uint32_t j0,
+                                                    uint32_t j1, const float4* part, uint32_t r,
+                                                    uint64_t grow, uint64_t gcol0) {
+  constexpr int NB = 8;
+  const float4* src = base_r + ra.slot0 * ra.slot_v;
+  for (uint32_t jb = ga; jb < j1; jb += 2 * NB) {
+    float4 q[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (jb + 2 * i < j1) q[i] = ld_cg_f4(src + (uint64_t)(jb + 2 * i) * kBM);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      if (jb + 2 * i < j1) {
+        float4 a = part[(jb + 2 * i - j0) * kBM + r];
+        a.x += q[i].x;
+        a.y += q[i].y;
+        a.z += q[i].z;
+        a.w += q[i].w;
+        store_vec4(p, grow, gcol0 + 4 * (jb + 2 * i), a);
+      }
+    }
+  }
+}
+
 // Hand an accumulator stage back to the MMA issuer (the rank-0 CTA's barrier).
 template <int CG>
 __device__ __forceinline__ void release_acc_t(uint64_t* bar) {
@@ -478,6 +563,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, descriptor prefetch) overlaps the previous kernel's tail; no
+  // global memory written by earlier work is touched before this wait.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) SKPP_STAMP(p, TL_START);
 
   if (warp == 0) {
@@ -731,78 +821,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       // contributor x0+t wrote its first Stream-K item (slot 2*cta), except x0
       // when its range starts inside an earlier tile (tile u is its last item)
       const uint64_t slot0 = 2 * (x0 * CG + rank) + (aligned ? 0 : 1);
-      for (uint32_t t = ft; t < nc; t += kThreads) {
-        const uint64_t sl = t == 0 ? slot0 : 2 * ((x0 + t) * CG + rank);
-        if (ld_acquire_gpu(p.flags + sl) != epoch) {
-          const long long t0 = clock64();
-          while (ld_acquire_gpu(p.flags + sl) != epoch) {
-            __nanosleep(32);
-            watchdog(t0, 5);
-          }
-        }
-      }
-      phase2_bar_sync();
-      if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
       const uint64_t tile = s.dp_tiles + u;
       const uint64_t grow = (tile / s.n_tiles) * TILE_M + rank * kBM + r;
       const uint64_t gcol0 = (tile % s.n_tiles) * BN;
-      for (uint32_t jb = j0; jb < j1; jb += 4) {
-        const uint32_t ga = jb + h, gb = jb + h + 2;
-        if (ga >= j1) continue;
-        const bool two = gb < j1;
-        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
-        const float4* base_a = wsv + (uint64_t)ga * kBM + r;
-        if (two) {
-          constexpr uint32_t KB = 8;
-          for (uint32_t t0 = 0; t0 < nc; t0 += KB) {
-            float4 q0[KB], q1[KB];
-#pragma unroll
-            for (uint32_t b = 0; b < KB; ++b) {
-              if (t0 + b < nc) {
-                const uint64_t sl = (t0 + b) == 0 ? slot0 : 2 * ((x0 + t0 + b) * CG + rank);
-                q0[b] = ld_cg_f4(base_a + sl * slot_v);
-                q1[b] = ld_cg_f4(base_a + sl * slot_v + 2 * kBM);
-              }
-            }
-#pragma unroll
-            for (uint32_t b = 0; b < KB; ++b) {
-              if (t0 + b < nc) {
-                acc0.x += q0[b].x;
-                acc0.y += q0[b].y;
-                acc0.z += q0[b].z;
-                acc0.w += q0[b].w;
-                acc1.x += q1[b].x;
-                acc1.y += q1[b].y;
-                acc1.z += q1[b].z;
-                acc1.w += q1[b].w;
-              }
-            }
-          }
-        } else {
-          constexpr uint32_t KB = 16;
-          for (uint32_t t0 = 0; t0 < nc; t0 += KB) {
-            float4 q0[KB];
-#pragma unroll
-            for (uint32_t b = 0; b < KB; ++b) {
-              if (t0 + b < nc) {
-                const uint64_t sl = (t0 + b) == 0 ? slot0 : 2 * ((x0 + t0 + b) * CG + rank);
-                q0[b] = ld_cg_f4(base_a + sl * slot_v);
-              }
-            }
-#pragma unroll
-            for (uint32_t b = 0; b < KB; ++b) {
-              if (t0 + b < nc) {
-                acc0.x += q0[b].x;
-                acc0.y += q0[b].y;
-                acc0.z += q0[b].z;
-                acc0.w += q0[b].w;
-              }
-            }
-          }
-        }
-        store_vec4(p, grow, gcol0 + 4 * ga, acc0);
-        if (two) store_vec4(p, grow, gcol0 + 4 * gb, acc1);
-      }
+      const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc};
+      const float4* base_r = wsv + r;  // this thread's row in every slot
+      float4* part = reinterpret_cast<float4*>(smem);  // idle operand ring: [group - j0][row]
+      // (a) the peers x0+1 .. x1 produce this tile as their FIRST item and are
+      //     ready early: sum them (in increasing CTA order) into shared memory
+      //     while x0, whose item may be its LAST, is still running.
+      for (uint32_t t = 1 + ft; t < nc; t += kThreads) wait_flag(p.flags + 2 * ((x0 + t) * CG + rank), epoch);
+      phase2_bar_sync();
+      if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
+      if (nc <= 4)
+        sum_peers<4, 3, CG>(ra, base_r, j0 + h, j0, j1, part, r);
+      else if (nc <= 7)
+        sum_peers<2, 6, CG>(ra, base_r, j0 + h, j0, j1, part, r);
+      else
+        sum_peers<1, 12, CG>(ra, base_r, j0 + h, j0, j1, part, r);
+      // (b) x0 last: fixed order (peers, then x0) => deterministic.
+      if (ft == 0) wait_flag(p.flags + slot0, epoch);
+      phase2_bar_sync();
+      add_owner_and_store(p, ra, base_r, j0 + h, j0, j1, part, r, grow, gcol0);
     }
     if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
     // ---- launch epilogue: the last CTA out advances the workspace epoch
@@ -918,6 +958,7 @@ static void sched_from_c(const skpp_sched_t& c, Sched& s) {
 
 static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
 static uint32_t g_l2_prefetch = 0;       // skpp_set_l2_prefetch
+static int g_pdl = 1;                    // skpp_set_pdl
 
 // A prepared launch: tensor maps, parameters and kernel, built once.
 struct Plan {
@@ -1076,6 +1117,7 @@ extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_til
 
 extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
 extern "C" void skpp_set_l2_prefetch(uint32_t k_blocks) { g_l2_prefetch = k_blocks; }
+extern "C" void skpp_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 
 extern "C" int skpp_set_device(int device) {
   cudaError_t e = cudaSetDevice(device);
@@ -1273,26 +1315,24 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = pl->smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   cfg.attrs = attr;
   cfg.numAttrs = 0;
+  if (g_pdl) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
+  }
   if (pl->cg == 2) {
     attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
     attr[cfg.numAttrs].val.clusterDim.x = 2;
     attr[cfg.numAttrs].val.clusterDim.y = 1;
     attr[cfg.numAttrs].val.clusterDim.z = 1;
     ++cfg.numAttrs;
-  } else if (pl->cs.sk_tiles > 0) {
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cap);
-    if (cap == cudaStreamCaptureStatusNone) {
-      // Stream-K contributors wait on each other: every CTA must be resident at once.
-      // (Cluster launches rely on the host-side co-residency check instead.)
-      attr[cfg.numAttrs].id = cudaLaunchAttributeCooperative;
-      attr[cfg.numAttrs].val.cooperative = 1;
-      ++cfg.numAttrs;
-    }
   }
+  // No cooperative attribute: no CTA waits before it has published all of its
+  // partials, and g never exceeds the co-resident CTAs (checked at plan time),
+  // so every waited-for CTA eventually runs; this keeps PDL overlap available.
   void* args[4] = {&pl->ma, &pl->mb, &pl->mc, &gp};
   cudaError_t e = cudaLaunchKernelExC(&cfg, pl->func, args);
   if (e != cudaSuccess) {

@@ -15,7 +15,10 @@ def main():
     a = torch.randn(128, 64, device="cuda").to(torch.bfloat16)
     b = torch.randn(64, 128, device="cuda").to(torch.bfloat16)
     c = torch.empty(128, 128, device="cuda")
-    for pol in (sk.Policy.data_parallel(), sk.Policy.all_stream_k()):
+    from paper_2408_11417_b200 import _lib
+
+    for pdl, pol in [(p, q) for p in (0, 1) for q in (sk.Policy.data_parallel(), sk.Policy.all_stream_k())]:
+        _lib.lib.skpp_set_pdl(pdl)
         plan = sk.GemmPlan(a, b, c, pol)
         for _ in range(20):
             plan.launch()
@@ -27,7 +30,7 @@ def main():
         t1 = time.perf_counter()
         torch.cuda.synchronize()
         t2 = time.perf_counter()
-        print(f"{pol.label}: host {1e6 * (t1 - t0) / n:.2f} us/launch, device-bound {1e6 * (t2 - t0) / n:.2f} us/launch")
+        print(f"pdl={pdl} {pol.label}: host {1e6 * (t1 - t0) / n:.2f} us/launch, device-bound {1e6 * (t2 - t0) / n:.2f} us/launch")
     x = torch.empty(1024, device="cuda")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
