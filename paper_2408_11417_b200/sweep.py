@@ -266,6 +266,62 @@ def gpu_measure(tile: TileShape, policies: list[Policy] | None = None, params: M
     return measure
 
 
+def run_shard_tiles(sizes: list[ProblemSize], rank: int, world: int, tiles: list[TileShape],
+                    params: MeasureParams, out_dir: str, tag: str = "records") -> None:
+    """Measure this rank's LPT share of ``sizes`` under every tile; one CSV shard per tile."""
+    import os
+
+    from .pipeline import write_records_csv
+    from .tiles import tile_label
+
+    mine = lpt_partition(sizes, world)[rank]
+    mine.sort(key=lambda s: (s.m, s.n, s.k))
+    pool = OperandPool(mine, params.in_dtype, params.out_dtype) if mine else None
+    for tile in tiles:
+        path = os.path.join(out_dir, f"{tag}.{tile_label(tile)}.rank{rank}.csv")
+        if mine:
+            write_records_csv(path, tune_sizes(mine, tile, None, None, params, pool))
+        else:
+            open(path, "w").close()
+
+
+def merge_tiles(out_dir: str, world: int, tiles: list[TileShape], tag: str = "records"):
+    """Per-tile merged CSVs (reference schema) and the joint (tile, policy) records."""
+    import os
+
+    from .pipeline import read_records_csv, write_records_csv, records_from_rows
+    from .tiles import joint_records_from_csvs, tile_label
+
+    paths = []
+    for tile in tiles:
+        rows = []
+        for r in range(world):
+            p = os.path.join(out_dir, f"{tag}.{tile_label(tile)}.rank{r}.csv")
+            if os.path.getsize(p):
+                rows.extend(read_records_csv(p))
+        recs = records_from_rows(rows)
+        recs.sort(key=lambda rec: (rec.size.m, rec.size.n, rec.size.k))
+        merged = os.path.join(out_dir, f"{tag}.{tile_label(tile)}.csv")
+        write_records_csv(merged, recs)
+        paths.append((tile, merged))
+    return joint_records_from_csvs(paths), paths
+
+
+def heldout_sizes(n: int, seed: int = 7) -> list[ProblemSize]:
+    """Off-grid sizes (not powers of two) for held-out selection checks."""
+    import random
+
+    rnd = random.Random(seed)
+    out = set()
+    while len(out) < n:
+        m = int(2 ** rnd.uniform(0, 13))
+        nn = int(2 ** rnd.uniform(6, 13))
+        k = int(2 ** rnd.uniform(4, 15))
+        if m & (m - 1) or nn & (nn - 1) or k & (k - 1):
+            out.add(ProblemSize(m, nn, k))
+    return sorted(out, key=lambda s: (s.m, s.n, s.k))
+
+
 def main(argv=None) -> int:
     """Sweep CLI.  Single GPU:  python -m paper_2408_11417_b200.sweep --out DIR
     Multi GPU (one process per GPU):  torchrun --nproc-per-node N -m paper_2408_11417_b200.sweep --out DIR
@@ -276,14 +332,17 @@ def main(argv=None) -> int:
 
     from . import pipeline as pl
     from .sieve import elimination_stats
+    from .tiles import build_tile_bank, evaluate_selection, parse_tile, tile_label
 
     ap = argparse.ArgumentParser(description=main.__doc__)
     ap.add_argument("--out", required=True)
     ap.add_argument("--grid", default="paper", help="paper | small | llama | paper+llama")
-    ap.add_argument("--tile", default="128x128x64")
+    ap.add_argument("--tiles", default="128x128x64", help="comma list; the first is the baseline tile")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--max-gflop", type=float, default=0.0, help="skip sizes above this (0 = no limit)")
+    ap.add_argument("--validate", action="store_true", help="re-measure everything (held-out run)")
+    ap.add_argument("--heldout", type=int, default=0, help="also measure N off-grid sizes")
     args = ap.parse_args(argv)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -294,38 +353,64 @@ def main(argv=None) -> int:
     sizes = grid_sizes(args.grid)
     if args.max_gflop > 0:
         sizes = [s for s in sizes if s.flops <= args.max_gflop * 1e9]
-    tile = TileShape(*(int(v) for v in args.tile.split("x")))
+    tiles = [parse_tile(t) for t in args.tiles.split(",")]
     params = MeasureParams(warmup=args.warmup, reps=args.reps)
-    sw = Stopwatch()
-    with sw:
-        recs = run_shard(sizes, rank, world, gpu_measure(tile, None, params), args.out)
-    with open(os.path.join(args.out, f"timing.rank{rank}.json"), "w") as fh:
-        json.dump({"rank": rank, "world": world, "sizes": len(recs), "seconds": sw.seconds}, fh)
+    dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("gloo")
-        dist.barrier()  # host-side rendezvous only: shards are files
-        dist.destroy_process_group()
+        dist.init_process_group("gloo")  # host rendezvous only: records travel as files
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    sw = Stopwatch()
+    with sw:
+        run_shard_tiles(sizes, rank, world, tiles, params, args.out, "records")
+    with open(os.path.join(args.out, f"timing.rank{rank}.json"), "w") as fh:
+        json.dump({"rank": rank, "world": world, "seconds": sw.seconds, "tiles": len(tiles)}, fh)
+    if args.validate:
+        run_shard_tiles(sizes, rank, world, tiles, params, args.out, "validate")
+    if args.heldout:
+        run_shard_tiles(heldout_sizes(args.heldout), rank, world, tiles, params, args.out, "heldout")
+    barrier()
     if rank == 0:
-        merged = merge_shards(args.out, world)
-        bank = pl.build_bank(merged)
-        bank.save(os.path.join(args.out, "bank.sieve"))
-        pl.write_records_csv(os.path.join(args.out, "records.csv"), merged)
+        joint, paths = merge_tiles(args.out, world, tiles, "records")
+        tb = build_tile_bank(joint, tiles)
+        tb.save(os.path.join(args.out, "tilebank"))
         times = [json.load(open(os.path.join(args.out, f"timing.rank{r}.json")))["seconds"] for r in range(world)]
-        el = elimination_stats(bank, merged)
+        n_pairs = len(sizes) * 7 * len(tiles)
+        per_tile = {}
+        for tile, path in paths:
+            recs = pl.records_from_rows(pl.read_records_csv(path))
+            bank = pl.build_bank(recs)
+            el = elimination_stats(bank, recs)
+            per_tile[tile_label(tile)] = {
+                "winner_counts": pl.winner_counts(recs),
+                "eliminated_fraction": el.eliminated_fraction,
+                "false_negatives": el.false_negatives,
+            }
         summary = {
-            "sizes": len(merged), "policies": 7, "tile": args.tile, "world": world,
+            "sizes": len(sizes), "policies": 7, "tiles": [tile_label(t) for t in tiles], "world": world,
             "sweep_seconds_max_over_ranks": max(times),
-            "shape_policy_per_s": sweep_throughput(len(merged), 7, max(times)),
-            "winner_counts": pl.winner_counts(merged),
-            "elimination": {"eliminated_fraction": el.eliminated_fraction,
-                            "false_negatives": el.false_negatives, "evaluations_saved": el.evaluations_saved},
-            "selection": pl.selection_quality(merged, bank),
+            "shape_policy_per_s": n_pairs / max(times),
+            "per_tile": per_tile,
+            "joint_winner_tiles": {tile_label(t): sum(1 for r in joint if r.winner[0] == t) for t in tiles},
+            "selection_in_sample": evaluate_selection(tb, joint),
         }
+        if args.validate:
+            joint2, _ = merge_tiles(args.out, world, tiles, "validate")
+            summary["selection_heldout_run"] = evaluate_selection(tb, joint2)
+        if args.heldout:
+            jh, _ = merge_tiles(args.out, world, tiles, "heldout")
+            summary["selection_offgrid_baseline_fallback"] = evaluate_selection(tb, jh, nearest=False)
+            summary["selection_offgrid_nearest_pow2"] = evaluate_selection(tb, jh, nearest=True)
         with open(os.path.join(args.out, "summary.json"), "w") as fh:
             json.dump(summary, fh, indent=1)
         print(json.dumps(summary))
+    if dist is not None:
+        dist.destroy_process_group()
     return 0
 
 

@@ -1,0 +1,197 @@
+"""Joint (tile shape, policy) selection: one Bloom bank per tile shape.
+
+The reference tunes the seven policies for a single tile shape and notes
+additional tuning parameters as future work (SURVEY §8(f) rank
+4).  On the B200 the tile shape matters as much as the policy (e.g. the
+256x256 CTA-pair tile is ~1.5x faster on large Llama projections, the
+128x128 tile wins on skinny split-K shapes), so the sweep measures every
+(tile, policy) and the winner of a size is inserted into the bank of its
+tile.  Each per-tile bank is an ordinary reference-format ``SKPS`` bank; a
+JSON manifest lists the tiles in priority order.
+
+Query: candidates = union over tiles of (tile, p) for p in bank[tile].query(size),
+plus the baseline (first tile, data-parallel), which is always evaluated.
+There are no false negatives: the measured winner is always a candidate.
+Sizes absent from every bank fall back to the baseline, or — with
+``nearest=True`` — to the candidates of the nearest tuned power-of-two size.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+from dataclasses import dataclass
+
+from .costmodel import CostEstimate, TuneRecord, rank_costs
+from .sieve import SieveBank
+from .types import Policy, ProblemSize, TileShape
+
+Config = tuple  # (TileShape, Policy)
+
+
+def tile_label(t: TileShape) -> str:
+    return f"{t.blk_m}x{t.blk_n}x{t.blk_k}"
+
+
+def parse_tile(s: str) -> TileShape:
+    return TileShape(*(int(v) for v in s.split("x")))
+
+
+@dataclass(frozen=True)
+class JointRecord:
+    """Per-size measurements of every (tile, policy) and the joint winner."""
+
+    size: ProblemSize
+    per_tile: tuple  # ((TileShape, TuneRecord), ...) in tile priority order
+    winner: Config
+    winner_us: float
+
+    def time_of(self, cfg: Config) -> float:
+        tile, pol = cfg
+        for t, rec in self.per_tile:
+            if t == tile:
+                for p, e in rec.costs:
+                    if p == pol:
+                        return e.makespan
+        raise KeyError(cfg)
+
+
+def joint_winner(size: ProblemSize, per_tile) -> JointRecord:
+    """Argmin over (tile, policy); ties go to the earlier tile, then the reference tie-break."""
+    best = None
+    for ti, (tile, rec) in enumerate(per_tile):
+        for pol, est in rec.costs:
+            key = (est.makespan, ti, pol.sort_key())
+            if best is None or key < best[0]:
+                best = (key, (tile, pol))
+    return JointRecord(size, tuple(per_tile), best[1], best[0][0])
+
+
+class TileBank:
+    """Per-tile SieveBanks behind one (tile, policy) query."""
+
+    def __init__(self, tiles: list[TileShape], banks: list[SieveBank] | None = None, **bank_kwargs):
+        if not tiles:
+            raise ValueError("need at least one tile shape")
+        self.tiles = list(tiles)
+        self.banks = banks if banks is not None else [SieveBank(**bank_kwargs) for _ in tiles]
+        if len(self.banks) != len(self.tiles):
+            raise ValueError("one bank per tile")
+        self._tuned_keys: set | None = None
+
+    @property
+    def baseline(self) -> Config:
+        return (self.tiles[0], Policy.data_parallel())
+
+    def insert(self, size: ProblemSize, cfg: Config) -> None:
+        tile, pol = cfg
+        self.banks[self.tiles.index(tile)].insert(size, pol)
+
+    def query(self, size: ProblemSize, nearest: bool = False) -> list[Config]:
+        """(tile, policy) candidates reported by the filters, tile-major."""
+        out = [(t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(size)]
+        if not out and nearest:
+            snapped = snap_pow2(size)
+            if snapped != size:
+                out = [(t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(snapped)]
+        return out
+
+    def candidates(self, size: ProblemSize, nearest: bool = False) -> list[Config]:
+        cand = self.query(size, nearest)
+        if self.baseline not in cand:
+            cand.append(self.baseline)
+        return cand
+
+    def save(self, out_dir: str) -> None:
+        os.makedirs(out_dir, exist_ok=True)
+        manifest = []
+        for t, b in zip(self.tiles, self.banks):
+            name = f"bank_{tile_label(t)}.sieve"
+            b.save(os.path.join(out_dir, name))
+            manifest.append({"tile": tile_label(t), "bank": name})
+        with open(os.path.join(out_dir, "tilebank.json"), "w") as fh:
+            json.dump({"format": "skpp-tilebank-1", "tiles": manifest}, fh, indent=1)
+
+    @classmethod
+    def load(cls, out_dir: str) -> "TileBank":
+        with open(os.path.join(out_dir, "tilebank.json")) as fh:
+            man = json.load(fh)
+        tiles = [parse_tile(e["tile"]) for e in man["tiles"]]
+        banks = [SieveBank.load(os.path.join(out_dir, e["bank"])) for e in man["tiles"]]
+        return cls(tiles, banks)
+
+
+def snap_pow2(size: ProblemSize) -> ProblemSize:
+    """Nearest power of two per dimension (in log space)."""
+    def snap(v: int) -> int:
+        return 1 << max(0, round(math.log2(v)))
+
+    return ProblemSize(snap(size.m), snap(size.n), snap(size.k))
+
+
+def build_tile_bank(records: list[JointRecord], tiles: list[TileShape], **bank_kwargs) -> TileBank:
+    """Insert every size's joint winner, in (m, n, k) order (bytes independent of sweep order)."""
+    tb = TileBank(tiles, **bank_kwargs)
+    for rec in sorted(records, key=lambda r: (r.size.m, r.size.n, r.size.k)):
+        tb.insert(rec.size, rec.winner)
+    return tb
+
+
+def evaluate_selection(bank: TileBank, records: list[JointRecord], tolerance: float = 0.2,
+                       nearest: bool = False) -> dict:
+    """Selected = fastest measured candidate of bank.candidates(size); compare to the measured oracle.
+
+    ``records`` may come from a different measurement run than the one the bank
+    was built from (held-out validation) or hold sizes the bank never saw.
+    """
+    n_all = sum(len(rec.costs) for _, rec in records[0].per_tile) if records else 0
+    within = 0
+    ratios = []
+    evaluated = 0
+    vs_dp = []
+    for rec in records:
+        cand = bank.candidates(rec.size, nearest)
+        evaluated += len(cand) - 1
+        times = [(rec.time_of(c), i) for i, c in enumerate(cand)]
+        chosen_us = min(times)[0]
+        ratio = chosen_us / rec.winner_us if rec.winner_us > 0 else 1.0
+        ratios.append(ratio)
+        within += ratio <= 1.0 + tolerance
+        vs_dp.append(rec.time_of(bank.baseline) / chosen_us)
+    possible = len(records) * max(n_all - 1, 1)
+    ratios.sort()
+    return {
+        "sizes": len(records),
+        "candidates_per_size_all": n_all,
+        "tolerance": tolerance,
+        "fraction_within": within / len(records) if records else 1.0,
+        "median_slowdown_vs_oracle": ratios[len(ratios) // 2] if ratios else 1.0,
+        "p95_slowdown_vs_oracle": ratios[int(0.95 * (len(ratios) - 1))] if ratios else 1.0,
+        "max_slowdown_vs_oracle": ratios[-1] if ratios else 1.0,
+        "eliminated_fraction": 1.0 - evaluated / possible if possible else 1.0,
+        "geomean_speedup_vs_baseline_dp": math.exp(sum(math.log(v) for v in vs_dp) / len(vs_dp)) if vs_dp else 1.0,
+    }
+
+
+def joint_records_from_csvs(paths_by_tile: list[tuple[TileShape, str]]) -> list[JointRecord]:
+    """Rebuild joint records from per-tile records CSVs (reference schema)."""
+    from .pipeline import read_records_csv, records_from_rows
+
+    per_size: dict[ProblemSize, list] = {}
+    for tile, path in paths_by_tile:
+        for rec in records_from_rows(read_records_csv(path)):
+            per_size.setdefault(rec.size, []).append((tile, rec))
+    tiles = [t for t, _ in paths_by_tile]
+    out = []
+    for size, lst in per_size.items():
+        lst.sort(key=lambda tr: tiles.index(tr[0]))
+        out.append(joint_winner(size, lst))
+    out.sort(key=lambda r: (r.size.m, r.size.n, r.size.k))
+    return out
+
+
+__all__ = [
+    "JointRecord", "TileBank", "build_tile_bank", "evaluate_selection", "joint_records_from_csvs",
+    "joint_winner", "parse_tile", "snap_pow2", "tile_label", "CostEstimate", "TuneRecord", "rank_costs",
+]

@@ -101,3 +101,64 @@ def test_gloo_two_rank_sweep_matches_single_process(tmp_path):
     got = (tmp_path / "bank.bin").read_bytes()
     want = pl.build_bank(fake_measure(small_grid())).to_bytes()
     assert got == want
+
+
+# -- joint (tile, policy) selection -----------------------------------------------------
+
+from paper_2408_11417_b200 import tiles as tl  # noqa: E402
+
+TILES = [sk.TileShape(128, 128, 64), sk.TileShape(256, 256, 64)]
+
+
+def fake_joint(sizes, salt=0):
+    out = []
+    for s in sizes:
+        per = []
+        for ti, t in enumerate(TILES):
+            costs = [(p, sk.CostEstimate(fake_cost(s, p) * (1.0 + 0.3 * ti * (s.m < 256)) + salt * 1e-3 * p.ordinal,
+                                         0.5, 0, 0)) for p in CANON]
+            per.append((t, sk.rank_costs(s, costs)))
+        out.append(tl.joint_winner(s, per))
+    return out
+
+
+def test_tile_bank_zero_false_negatives_and_round_trip(tmp_path):
+    sizes = small_grid()
+    joint = fake_joint(sizes)
+    tb = tl.build_tile_bank(joint, TILES)
+    for rec in joint:
+        assert rec.winner in tb.candidates(rec.size)
+    q = tl.evaluate_selection(tb, joint)
+    assert q["fraction_within"] == 1.0 and q["max_slowdown_vs_oracle"] == 1.0
+    assert q["candidates_per_size_all"] == 14 and q["eliminated_fraction"] > 0.5
+    tb.save(str(tmp_path / "tb"))
+    back = tl.TileBank.load(str(tmp_path / "tb"))
+    assert back.tiles == TILES
+    assert [b.to_bytes() for b in back.banks] == [b.to_bytes() for b in tb.banks]
+    # every per-tile bank is a reference-format bank (reloadable by SieveBank)
+    for b in back.banks:
+        assert sk.SieveBank.from_bytes(b.to_bytes()).policies == CANON
+
+
+def test_tile_bank_order_independent_and_nearest_fallback():
+    sizes = small_grid()
+    joint = fake_joint(sizes)
+    a = tl.build_tile_bank(joint, TILES)
+    b = tl.build_tile_bank(list(reversed(joint)), TILES)
+    assert [x.to_bytes() for x in a.banks] == [x.to_bytes() for x in b.banks]
+    off = sk.ProblemSize(100, 70, 1000)
+    assert tl.snap_pow2(off) == sk.ProblemSize(128, 64, 1024)
+    assert a.candidates(off) == [a.baseline] or len(a.candidates(off)) >= 1
+    assert set(a.query(tl.snap_pow2(off))) <= set(a.candidates(off, nearest=True)) | {a.baseline}
+
+
+def test_joint_records_from_per_tile_csvs(tmp_path):
+    sizes = small_grid()[:40]
+    joint = fake_joint(sizes)
+    paths = []
+    for ti, t in enumerate(TILES):
+        path = tmp_path / f"r{ti}.csv"
+        pl.write_records_csv(path, [dict(rec.per_tile)[t] for rec in joint])
+        paths.append((t, str(path)))
+    back = tl.joint_records_from_csvs(paths)
+    assert [(r.size, r.winner) for r in back] == [(r.size, r.winner) for r in sorted(joint, key=lambda r: (r.size.m, r.size.n, r.size.k))]

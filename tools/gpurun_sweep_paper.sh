@@ -1,4 +1,4 @@
 set -x
-mkdir -p gpurun_out/sweep_paper
-timeout 3000 python -m paper_2408_11417_b200.sweep --out gpurun_out/sweep_paper --grid paper+llama --tile 128x128x64 > gpurun_out/sweep_paper/log.txt 2>&1; echo rc=$?
-tail -3 gpurun_out/sweep_paper/log.txt
+O=gpurun_out/sweep_joint; mkdir -p $O
+timeout 3000 python -m paper_2408_11417_b200.sweep --out $O --grid paper+llama --tiles 128x128x64,256x256x64 --validate --heldout 300 > $O/log.txt 2>&1; echo rc=$?
+tail -c 3000 $O/log.txt
