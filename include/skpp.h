@@ -134,13 +134,13 @@ int skpp_set_device(int device);
    (setup done, first load, first stage landed, last MMA, items done, flags seen,
    reductions done, ...) to device_buffer[cta*16 + event].  NULL disables. */
 void skpp_debug_timeline(uint64_t* device_buffer);
-/* Tuning knob for launches made after the call: the TMA producer also prefetches
-   into L2 the k-blocks up to `k_blocks` ahead of the one it loads (0 = off). */
-void skpp_set_l2_prefetch(uint32_t k_blocks);
 /* Programmatic dependent launch (default on): a GEMM launched right after another
    kernel runs its prologue (barriers, TMEM, descriptors) under that kernel's tail
    and waits (griddepcontrol.wait) before touching global memory. */
 void skpp_set_pdl(int enable);
+/* Load each stage's B columns with one 3-D TMA box when N % 64 == 0 (default on;
+   plans created after the call). */
+void skpp_set_b3d(int enable);
 /* SM count, compute capability and the co-resident CTA limit of the GEMM kernel for blk_n. */
 int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 int skpp_max_coresident(const skpp_tile_t* t, int32_t* ctas);

@@ -108,11 +108,22 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
+// 3-D box: (n within a 64-column chunk, k, chunk) -> smem [chunk][k][64]
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int32_t c0,
+                                                 int32_t c1, int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0,
                                              int32_t c1) {
@@ -325,7 +336,7 @@ struct GemmParams {
   uint64_t trace_cap;
   int64_t* trace_counts;
   uint64_t* timeline;  // debug: TL_EVENTS %globaltimer stamps per CTA, or null
-  uint32_t l2_prefetch; // k-blocks ahead to prefetch into L2 (0 = off)
+  uint32_t b3d;         // tmB is the 3-D (n64, k, chunk) map: one B load per stage
 };
 
 // Debug timeline (skpp_debug_timeline): per-CTA %globaltimer stamps.
@@ -347,6 +358,15 @@ __device__ __forceinline__ uint64_t gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Per-k-block stamps of CTA 0 (issue by the producer, arrival seen by the MMA
+// warp) in SM clock cycles (clock64; %globaltimer reads are too slow here),
+// after the per-CTA table: timeline[gridDim.x*TL_EVENTS + 2*k + {0,1}].
+constexpr int TL_KSTAMPS = 256;
+#define SKPP_KSTAMP(p, k, which)                                                          \
+  do {                                                                                    \
+    if ((p).timeline && blockIdx.x == 0 && (k) < TL_KSTAMPS)                              \
+      (p).timeline[(uint64_t)gridDim.x * TL_EVENTS + 2 * (k) + (which)] = clock64();      \
+  } while (0)
 #define SKPP_STAMP(p, ev) \
   do { if ((p).timeline) (p).timeline[(uint64_t)blockIdx.x * TL_EVENTS + (ev)] = gtimer(); } while (0)
 
@@ -529,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (uint32_t i = 0; i < C::STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
+      mbar_init(&full_bar[i], 2);  // the A and the B producer
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -570,61 +590,68 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) SKPP_STAMP(p, TL_START);
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer (1 lane)
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      bool first_load = true;
-      Cursor cur;
-      cursor_init(cur, s, x);
-      Item it;
-      while (cursor_next(cur, s, x, it)) {
-        const int32_t m0 = (int32_t)((it.tile / s.n_tiles) * TILE_M + rank * kBM);
-        const int32_t n0 = (int32_t)((it.tile % s.n_tiles) * BN + rank * C::BNC);
-        for (uint64_t kk = it.kb; kk < it.ke; ++kk) {
-          mbar_wait(&empty_bar[stage], phase ^ 1, 1);
-          // the MMA-issuing (rank-0) CTA's barrier expects the bytes of the whole pair
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * C::STAGE_BYTES);
+  if ((warp == 0 || warp == 3) && lane == 0) {
+    // ------------------------------------------------ TMA producers
+    // Two issuing threads — warp 0 loads A, warp 3 loads B — because a single
+    // thread's wait + expect_tx + TMA issue sequence (~250 ns per stage) is a
+    // throughput limit of its own; each arrives once per stage on the full
+    // barrier with its own byte count.
+    const bool load_a = warp == 0;
+    uint32_t stage = 0, phase = 0, kcount = 0;
+    bool first_load = true;
+    Cursor cur;
+    cursor_init(cur, s, x);
+    Item it;
+    while (cursor_next(cur, s, x, it)) {
+      const int32_t m0 = (int32_t)((it.tile / s.n_tiles) * TILE_M + rank * kBM);
+      const int32_t n0 = (int32_t)((it.tile % s.n_tiles) * BN + rank * C::BNC);
+      for (uint64_t kk = it.kb; kk < it.ke; ++kk) {
+        mbar_wait(&empty_bar[stage], phase ^ 1, 1);
+        if (load_a) {
+          SKPP_KSTAMP(p, kcount, 0);
+          ++kcount;
           if (first_load) {
             SKPP_STAMP(p, TL_FIRST_TMA);
             first_load = false;
           }
-          const int32_t k0 = (int32_t)(kk * BK);
-          if constexpr (CG == 1) {
+        }
+        // the MMA-issuing (rank-0) CTA's barrier expects the bytes of the whole pair
+        if (rank == 0)
+          mbar_arrive_expect_tx(&full_bar[stage], CG * (load_a ? C::A_BYTES : C::B_BYTES));
+        const int32_t k0 = (int32_t)(kk * BK);
+        if constexpr (CG == 1) {
+          if (load_a) {
             tma_load_2d(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
+          } else if (p.b3d) {  // all of the stage's B columns in one 3-D box
+            tma_load_3d(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
+          } else {
 #pragma unroll
             for (int j = 0; j < C::BNC / 64; ++j)
               tma_load_2d(sB + stage * C::B_BYTES + j * (BK * 128), &tmB, n0 + 64 * j, k0,
                           &full_bar[stage]);
-          } else {
+          }
+        } else {
+          if (load_a) {
             tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
+          } else if (p.b3d) {
+            tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
+          } else {
 #pragma unroll
             for (int j = 0; j < C::BNC / 64; ++j)
               tma_load_2d_pair(sB + stage * C::B_BYTES + j * (BK * 128), &tmB, n0 + 64 * j, k0,
                                &full_bar[stage]);
           }
-          if (p.l2_prefetch) {
-            // warm L2 with the k-blocks beyond the ring: up to p.l2_prefetch of them
-            const uint64_t far = kk + C::STAGES + p.l2_prefetch - 1;
-            const uint64_t near = (kk == it.kb) ? kk + C::STAGES : far;
-            for (uint64_t kq = near; kq <= far && kq < it.ke; ++kq) {
-              const int32_t kq0 = (int32_t)(kq * BK);
-              tma_prefetch_2d(&tmA, kq0, m0);
-#pragma unroll
-              for (int j = 0; j < C::BNC / 64; ++j) tma_prefetch_2d(&tmB, n0 + 64 * j, kq0);
-            }
-          }
-          if (++stage == C::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (1 lane of the rank-0 CTA)
     if (lane == 0 && rank == 0) {
-      uint32_t stage = 0, phase = 0, local = 0;
+      uint32_t stage = 0, phase = 0, local = 0, kcount = 0;
       Cursor cur;
       cursor_init(cur, s, x);
       Item it;
@@ -636,6 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint64_t kk = it.kb; kk < it.ke; ++kk) {
           mbar_wait(&full_bar[stage], phase, 3);
           tc_fence_after();
+          SKPP_KSTAMP(p, kcount, 1);
+          ++kcount;
           if (local == 0 && kk == it.kb) SKPP_STAMP(p, TL_FIRST_FULL);
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -957,8 +986,8 @@ static void sched_from_c(const skpp_sched_t& c, Sched& s) {
 }
 
 static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
-static uint32_t g_l2_prefetch = 0;       // skpp_set_l2_prefetch
 static int g_pdl = 1;                    // skpp_set_pdl
+static int g_b3d = 1;                    // skpp_set_b3d
 
 // A prepared launch: tensor maps, parameters and kernel, built once.
 struct Plan {
@@ -1116,8 +1145,8 @@ extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_til
 }
 
 extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
-extern "C" void skpp_set_l2_prefetch(uint32_t k_blocks) { g_l2_prefetch = k_blocks; }
 extern "C" void skpp_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
+extern "C" void skpp_set_b3d(int enable) { g_b3d = enable ? 1 : 0; }
 
 extern "C" int skpp_set_device(int device) {
   cudaError_t e = cudaSetDevice(device);
@@ -1243,9 +1272,28 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
                                              : CU_TENSOR_MAP_SWIZZLE_32B;
   const CUtensorMapDataType in_dt = map_dtype(ops->in_dtype);
   rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK, kBM, aswz);
-  if (!rc)
+  const uint32_t bnc = t->blk_n / (t->blk_m / kBM);  // B columns per CTA
+  const bool b3d = g_b3d && p->n % 64 == 0 && bnc > 64;
+  if (!rc && b3d) {
+    // (n in chunk, k, chunk) view of B: one TMA op per stage fills [chunk][k][64];
+    // only when N is a multiple of 64, so no chunk reads past a row.
+    auto fn = encode_fn();
+    const cuuint64_t dims[3] = {64, p->k, p->n / 64};
+    const cuuint64_t strides[2] = {(cuuint64_t)ops->ldb * 2, 128};
+    const cuuint32_t box[3] = {64, BK, bnc / 64};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn ? fn(&pl->mb, in_dt, 3, const_cast<void*>(ops->b), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+                    : CUDA_ERROR_NOT_SUPPORTED;
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (3-D B) failed with CUresult " + std::to_string((int)r));
+      rc = SKPP_ELAUNCH;
+    }
+  } else if (!rc) {
     rc = make_map(&pl->mb, ops->b, in_dt, 2, p->n, p->k, (uint64_t)ops->ldb, 64, BK,
                   CU_TENSOR_MAP_SWIZZLE_128B);
+  }
   if (rc) {
     delete pl;
     return rc;
@@ -1258,6 +1306,7 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   gp.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (0u << 15) | (1u << 16) |
              ((uint32_t)(t->blk_n >> 3) << 17) | ((uint32_t)(t->blk_m >> 4) << 24);
   gp.out_dtype = ops->out_dtype;
+  gp.b3d = b3d ? 1 : 0;
   gp.C = ops->c;
   gp.ldc = (uint64_t)ops->ldc;
   const uint32_t esz = ops->out_dtype == SKPP_F32 ? 4 : 2;
@@ -1307,7 +1356,6 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
     }
   }
   gp.timeline = g_timeline;
-  gp.l2_prefetch = g_l2_prefetch;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));

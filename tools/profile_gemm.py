@@ -37,12 +37,16 @@ def main() -> None:
     ap.add_argument("--out", default="fp32")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--flush", action="store_true", help="write 256 MiB between launches")
+    ap.add_argument("--b3d", type=int, default=1, help="one 3-D TMA box for B per stage")
     args = ap.parse_args()
 
     import torch
 
     import paper_2408_11417_b200 as sk
 
+    from paper_2408_11417_b200 import _lib
+
+    _lib.lib.skpp_set_b3d(args.b3d)
     dt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
     od = {"fp32": torch.float32, "bf16": torch.bfloat16, "fp16": torch.float16}[args.out]
     tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
@@ -62,7 +66,7 @@ def main() -> None:
     us = [ev[2 * i].elapsed_time(ev[2 * i + 1]) * 1e3 for i in range(args.iters)]
     fl = 2.0 * args.m * args.n * args.k
     best = min(us)
-    print(f"{args.m}x{args.n}x{args.k} {args.policy} tile {args.tile}: min {best:.2f} us "
+    print(f"{args.m}x{args.n}x{args.k} {args.policy} tile {args.tile} b3d={args.b3d}: min {best:.2f} us "
           f"median {sorted(us)[len(us)//2]:.2f} us -> {fl / best / 1e6:.1f} TFLOP/s")
 
 

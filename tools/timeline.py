@@ -21,7 +21,7 @@ def main() -> None:
     ap.add_argument("--policy", default="ask")
     ap.add_argument("--flush", action="store_true")
     ap.add_argument("--per-cta", type=int, default=0, help="print the first N CTAs")
-    ap.add_argument("--prefetch", type=int, default=0, help="L2 prefetch depth (k-blocks)")
+    ap.add_argument("--kstamps", type=int, default=0, help="print CTA 0's first N k-block stamps")
     args = ap.parse_args()
 
     import torch
@@ -34,9 +34,9 @@ def main() -> None:
     a = torch.randn(args.m, args.k, device="cuda").to(torch.bfloat16)
     b = torch.randn(args.k, args.n, device="cuda").to(torch.bfloat16)
     c = torch.empty(args.m, args.n, device="cuda")
-    _lib.lib.skpp_set_l2_prefetch(args.prefetch)
     plan = sk.GemmPlan(a, b, c, parse_policy(sk, args.policy), tile)
-    tl = torch.zeros(plan.g * 16, dtype=torch.int64, device="cuda")
+    grid = plan.g * (tile.blk_m // 128)
+    tl = torch.zeros(grid * 16 + 512, dtype=torch.int64, device="cuda")
     flush = torch.empty(64 << 20, device="cuda")
     for _ in range(3):
         plan.launch()
@@ -51,10 +51,12 @@ def main() -> None:
     e1.record()
     torch.cuda.synchronize()
     _lib.lib.skpp_debug_timeline(None)
-    t = tl.view(plan.g, 16).cpu().numpy().astype("float64")
+    raw = tl.cpu().numpy().astype("float64")
+    t = raw[: grid * 16].reshape(grid, 16)
+    ks = raw[grid * 16:].reshape(256, 2)
     base = t[:, 0][t[:, 0] > 0].min()
     print(f"{args.m}x{args.n}x{args.k} {args.policy} tile {args.tile} flush={args.flush}: "
-          f"prefetch={args.prefetch} event time {e0.elapsed_time(e1) * 1e3:.1f} us, "
+          f"event time {e0.elapsed_time(e1) * 1e3:.1f} us, "
           f"kernel span {(t[:, :11].max() - base) / 1e3:.2f} us")
     for i, name in enumerate(EVENTS):
         if name == "-":
@@ -64,6 +66,18 @@ def main() -> None:
         if len(col):
             print(f"  {name:>10}: min {col.min() / 1e3:8.2f}  med {sorted(col)[len(col) // 2] / 1e3:8.2f}  "
                   f"max {col.max() / 1e3:8.2f} us  (n={len(col)})")
+    if args.kstamps:
+        n = int((ks[:, 1] > 0).sum())
+        c0 = ks[0, 0]
+        print(f"  CTA 0 k-blocks: {n}; SM cycles relative to the first issue:")
+        for k in range(min(n, args.kstamps)):
+            lat = ks[k, 1] - ks[k, 0]
+            gap = ks[k, 1] - ks[k - 1, 1] if k else 0.0
+            igap = ks[k, 0] - ks[k - 1, 0] if k else 0.0
+            print(f"    k {k:3d}: issue {ks[k, 0] - c0:8.0f} (+{igap:5.0f}) arrive {ks[k, 1] - c0:8.0f} "
+                  f"(+{gap:5.0f}) lat {lat:6.0f}")
+        if n > 8:
+            print(f"  mean arrival spacing k>=8: {(ks[n - 1, 1] - ks[8, 1]) / (n - 9):.0f} cycles")
     for x in range(min(args.per_cta, plan.g)):
         row = [(t[x, i] - base) / 1e3 if t[x, i] > 0 else float('nan') for i in range(7)]
         print(f"  cta {x:3d}: " + " ".join(f"{v:7.2f}" for v in row))

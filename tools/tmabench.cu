@@ -24,7 +24,7 @@ __device__ __forceinline__ void wait_bar(uint64_t* b, uint32_t ph) {
 }
 
 template <int OPS>
-__global__ void ring_kernel(const __grid_constant__ CUtensorMap tm, int iters, int stages) {
+__global__ void ring_kernel(const __grid_constant__ CUtensorMap tm, int iters, int stages, int rows) {
   extern __shared__ __align__(1024) char sm[];
   __shared__ __align__(8) uint64_t full[16];
   if (threadIdx.x != 0) return;
@@ -32,7 +32,7 @@ __global__ void ring_kernel(const __grid_constant__ CUtensorMap tm, int iters, i
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   constexpr int CH = 4 / OPS;  // chunks per op
   uint32_t phase[16] = {0};
-  const int rows_total = 4096;  // 64 rows per k-block; tensor has 4096 rows x 16 chunks
+  const int rows_total = rows;
   for (int it = 0; it < iters + stages; ++it) {
     const int s = it % stages;
     if (it >= stages) {
@@ -66,11 +66,16 @@ int main() {
   cudaMemset(buf, 0, 64ull << 20);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int row_stride : {128, 1024, 8192, 32768})
   for (int ops : {1, 2, 4}) {
+    if (row_stride != 128 && ops != 2) continue;
     CUtensorMap tm;
     const int ch = 4 / ops;
-    cuuint64_t dims[3] = {64, 4096, 16};
-    cuuint64_t strides[2] = {128, 128ull * 4096};
+    // rows of 128 B at `row_stride`; 16 "chunks" of 64 columns side by side in a row
+    // when row_stride >= 2 KiB, else stacked (contiguous case)
+    const int rows = row_stride >= 2048 ? (int)((64ull << 20) / row_stride) : 4096;
+    cuuint64_t dims[3] = {64, (cuuint64_t)rows, 16};
+    cuuint64_t strides[2] = {(cuuint64_t)row_stride, row_stride >= 2048 ? 128ull : 128ull * 4096};
     cuuint32_t box[3] = {64, 64, (cuuint32_t)ch};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es,
@@ -80,11 +85,11 @@ int main() {
       printf("encode failed %d\n", (int)r);
       return 1;
     }
-    for (int stages : {2, 4, 6}) {
+    for (int stages : {4, 6}) {
       for (int grid : {1, sms}) {
         const int iters = 2000;
         const size_t smem = 32768 * stages;
-        void (*k)(CUtensorMap, int, int) = ops == 1 ? ring_kernel<1> : ops == 2 ? ring_kernel<2> : ring_kernel<4>;
+        void (*k)(CUtensorMap, int, int, int) = ops == 1 ? ring_kernel<1> : ops == 2 ? ring_kernel<2> : ring_kernel<4>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaEvent_t a, b;
         cudaEventCreate(&a);
@@ -92,7 +97,7 @@ int main() {
         float best = 1e30f;
         for (int rep = 0; rep < 4; ++rep) {
           cudaEventRecord(a);
-          k<<<grid, 32, smem>>>(tm, iters, stages);
+          k<<<grid, 32, smem>>>(tm, iters, stages, rows - 64);
           cudaEventRecord(b);
           cudaEventSynchronize(b);
           float ms;
@@ -100,8 +105,8 @@ int main() {
           if (rep && ms < best) best = ms;
         }
         cudaError_t e = cudaGetLastError();
-        printf("ops/stage %d (box %5d B) stages %d grid %3d: %7.1f GB/s per CTA, %8.1f GB/s total  %s\n", ops,
-               32768 / ops, stages, grid, 32768.0 * iters / best / 1e6, 32768.0 * iters * grid / best / 1e6,
+        printf("row_stride %6d ops/stage %d (box %5d B) stages %d grid %3d: %7.1f GB/s per CTA, %8.1f GB/s total  %s\n", ops,
+               row_stride, 32768 / ops, stages, grid, 32768.0 * iters / best / 1e6, 32768.0 * iters * grid / best / 1e6,
                e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
     }
