@@ -61,6 +61,15 @@ def sched_digest(rows) -> str:
     return hashlib.sha256(txt.encode()).hexdigest()
 
 
+def _tmp_csv(text: str) -> str:
+    import tempfile
+
+    fd, path = tempfile.mkstemp(suffix=".csv")
+    with os.fdopen(fd, "w") as fh:
+        fh.write(text)
+    return path
+
+
 def main() -> None:
     rng = np.random.default_rng(20240821)
     out: dict = {"generator": "tests/golden/make_golden.py", "reference": "gemmsched 0.1.0 (pkg/src/gemmsched)"}
@@ -263,6 +272,15 @@ def main() -> None:
         ordered = sorted(costs, key=lambda pc: (pc[1], pc[0].sort_key()))
         ranks.append([[c for _, c in costs], ordered[0][0].ordinal, ordered[1][0].ordinal])
     out["ranking"] = ranks
+
+    # -- records CSV + report of a small cost-model tune (reference pipeline.py:149-313)
+    small = G.gen_problem_grid(G.GridSpec(G.AxisRange(1, 256), G.AxisRange(64, 256), G.AxisRange(16, 1024)))
+    recs_small = G.tune_grid(small, G.TileShape(64, 64, 32), G.HardwareModel(13, 1))
+    out["report_case"] = {
+        "records_csv": G.records_csv_text(recs_small),
+        "report": G.build_report(G.read_records_csv(_tmp_csv(G.records_csv_text(recs_small)))),
+        "report_tol": G.build_report(G.read_records_csv(_tmp_csv(G.records_csv_text(recs_small))), [0.0, 0.3]),
+    }
 
     with open(OUT, "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
