@@ -153,6 +153,27 @@ def ncu_traffic(workload: str):
         return None, None
 
 
+def sweep_summary():
+    """Selection quality over the paper grid from the committed GPU sweep run (separate job)."""
+    path = os.path.join(ROOT, "profiles", "round1", "sweep_joint_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    held = d.get("selection_heldout_run", {})
+    off = d.get("selection_offgrid_nearest_pow2", {})
+    return {
+        "source": os.path.relpath(path, ROOT) + " (separate sweep job on the same GPU pool)",
+        "sizes": d.get("sizes"),
+        "tiles": d.get("tiles"),
+        "pct_within_20pct_of_oracle_heldout_run": round(100 * held.get("fraction_within", float("nan")), 2),
+        "pct_within_20pct_of_oracle_offgrid_sizes": round(100 * off.get("fraction_within", float("nan")), 2),
+        "eliminated_fraction": held.get("eliminated_fraction"),
+        "shape_policy_per_s_1gpu": round(d.get("shape_policy_per_s", 0.0), 1),
+    }
+
+
 def roofline(flops: float, nbytes: float, seconds: float, peaks: dict) -> dict:
     t_tc = flops / (peaks["bf16_tflops"] * 1e12)
     t_hbm = nbytes / (peaks["hbm_gbs"] * 1e9)
@@ -369,6 +390,7 @@ def run_ours(args, wl: dict) -> None:
                 "note": "per-policy times from CUDA-graph replays with warm L2 (selection sweep)",
             },
             "roofline": roof,
+            "sweep": sweep_summary(),
             "cpu_baseline": {
                 "value": round(cpu_value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
                 "sample": f"{len(cpu_times)} full {m}x{n}x{k} runs of the oracle port of gemmsched "
