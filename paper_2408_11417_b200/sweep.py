@@ -343,7 +343,12 @@ def main(argv=None) -> int:
     ap.add_argument("--max-gflop", type=float, default=0.0, help="skip sizes above this (0 = no limit)")
     ap.add_argument("--validate", action="store_true", help="re-measure everything (held-out run)")
     ap.add_argument("--heldout", type=int, default=0, help="also measure N off-grid sizes")
+    ap.add_argument("--emulate-world", default="",
+                    help="comma list of world sizes: run every rank's LPT share back to back on this GPU "
+                         "and report max-over-ranks time per world size (single-GPU scaling estimate)")
     args = ap.parse_args(argv)
+    if args.emulate_world:
+        return emulate_worlds(args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -411,6 +416,54 @@ def main(argv=None) -> int:
         print(json.dumps(summary))
     if dist is not None:
         dist.destroy_process_group()
+    return 0
+
+
+def emulate_worlds(args) -> int:
+    """Per-world-size sweep time when ranks run their LPT shares independently (no comms).
+
+    Each rank's share is measured separately on this GPU (one process, back to
+    back); a world of N GPUs would take max-over-ranks of those times, since
+    the shares share nothing.  Results are labelled as emulated.
+    """
+    import json
+    import os
+
+    from .tiles import parse_tile, tile_label
+
+    os.makedirs(args.out, exist_ok=True)
+    sizes = grid_sizes(args.grid)
+    if args.max_gflop > 0:
+        sizes = [s for s in sizes if s.flops <= args.max_gflop * 1e9]
+    tiles = [parse_tile(t) for t in args.tiles.split(",")]
+    params = MeasureParams(warmup=args.warmup, reps=args.reps)
+    pool = OperandPool(sizes, params.in_dtype, params.out_dtype)
+    # warm the process (kernel setup, allocator) so rank 0 is not charged for it
+    tune_sizes(sizes[:3], tiles[0], None, None, params, pool)
+    out = {"mode": "emulated: each rank's share measured back to back on one GPU; "
+                   "wall time of a world = max over its ranks", "sizes": len(sizes),
+           "tiles": [tile_label(t) for t in tiles], "policies": 7, "worlds": {}}
+    for world in (int(w) for w in args.emulate_world.split(",")):
+        parts = lpt_partition(sizes, world)
+        secs = []
+        for part in parts:
+            part = sorted(part, key=lambda s: (s.m, s.n, s.k))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for tile in tiles:
+                tune_sizes(part, tile, None, None, params, pool)
+            torch.cuda.synchronize()
+            secs.append(time.perf_counter() - t0)
+        pairs = len(sizes) * 7 * len(tiles)
+        out["worlds"][str(world)] = {
+            "rank_seconds": [round(v, 3) for v in secs],
+            "max_rank_seconds": round(max(secs), 3),
+            "shape_policy_per_s": round(pairs / max(secs), 1),
+            "load_imbalance": round(max(secs) / (sum(secs) / len(secs)), 3),
+        }
+        print(json.dumps({world: out["worlds"][str(world)]}), flush=True)
+    with open(os.path.join(args.out, "scaling_emulated.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
     return 0
 
 
