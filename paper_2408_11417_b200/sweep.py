@@ -177,11 +177,23 @@ def tune_sizes(
     return out
 
 
-def estimated_cost_s(size: ProblemSize, n_policies: int = 7, peak_tflops: float = 1200.0,
-                     launch_us: float = 8.0, reps: int = 13) -> float:
-    """Rough wall time of measuring one size (for LPT partitioning)."""
-    per = size.flops / (peak_tflops * 1e12) + launch_us * 1e-6
-    return n_policies * reps * per
+def estimated_cost_s(size: ProblemSize, n_policies: int = 7, peak_tflops: float = 1000.0,
+                     launch_us: float = 8.0, fixed_s: float = 2.5e-3, sms: int = 148,
+                     tile_mn: int = 128) -> float:
+    """Wall time of measuring one size with :func:`measure_size` (for LPT partitioning).
+
+    Models what a measurement does: per distinct schedule a fixed host cost
+    (plan, graph capture/instantiate) plus warm-up, one estimate launch and
+    ``reps`` graph replays of ``inner`` launches, with the same adaptive
+    inner/reps rules as :func:`time_plan`.  Small grids (fewer tiles than SMs)
+    have only two distinct schedules (every Stream-K policy is all-Stream-K).
+    """
+    t_us = size.flops / (peak_tflops * 1e6) + launch_us
+    inner = max(1, min(64, int(200.0 // t_us)))
+    reps = min(10, max(3, math.ceil(20000.0 / (inner * t_us))))
+    tiles = -(-size.m // tile_mn) * -(-size.n // tile_mn)
+    distinct = 2 if tiles <= sms else n_policies
+    return distinct * (fixed_s + (4 + inner * (1 + reps)) * t_us * 1e-6)
 
 
 def lpt_partition(sizes: list[ProblemSize], world: int, cost=estimated_cost_s) -> list[list[ProblemSize]]:
