@@ -10,10 +10,10 @@ the Stream-K++ selection layer picks:
      the device (identical schedules once), a Bloom bank is built from the
      winner, and the selected policy is the fastest measured candidate of
      ``bank.query(size) | {data-parallel}``;
-  2. timed region: K steps, one persistent-kernel launch per step, L2
-     flushed before every step (256 MiB write, then a 256 MiB read so the
-     resident lines are clean) outside the per-step CUDA events; device time
-     is the sum of per-step event times, max over ranks.
+  2. timed region: K steps, one persistent-kernel launch per step, back to
+     back on one stream between ONE pair of CUDA events (max over ranks);
+     the steps rotate over R distinct operand sets whose total is > 4x the
+     126 MB L2, so every step reads its operands from HBM (cold L2).
 
 Also reported: ``e2e`` (the same GEMM through the public
 ``execute_schedule`` with pinned host bf16 inputs, H2D + kernel + D2H every
@@ -43,6 +43,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 METRIC = "GEMM TFLOP/s vs dense TC peak; % shapes within 20% of oracle policy"
+ROTATE_BYTES = 4 * 128 * 1024 * 1024  # operand sets rotated through per step: 4x the 126 MB L2
+ISOLATED_STEPS = 50
 
 WORKLOADS = {
     "cfg2": dict(m=512, n=512, k=16384, dtype="bf16", tile=(128, 128, 64),
@@ -71,40 +73,66 @@ def load_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs.
 
-    def __init__(self, gpu_index: int, period_ms: int = 50):
+    A reader thread stamps every sample on arrival; ``summary`` keeps the samples
+    that arrived between ``mark_start()`` and ``mark_end()`` (plus one period), so
+    the idle lead-in needed to start nvidia-smi does not dilute the median.
+    """
+
+    def __init__(self, gpu_index: int, period_ms: int = 20):
         self.cmd = [
             "nvidia-smi", f"--id={gpu_index}",
             "--query-gpu=clocks.sm,clocks.max.sm,power.draw," + ",".join(
                 f"clocks_event_reasons.{r}" for r in REASON_FIELDS),
             "--format=csv,noheader,nounits", f"-lms={period_ms}",
         ]
+        self.period = period_ms / 1e3
         self.proc = None
+        self.samples: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
+
+    def _reader(self):
+        for ln in self.proc.stdout:
+            if ln.strip():
+                self.samples.append((time.time(), ln))
 
     def __enter__(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(self.cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._reader, daemon=True)
+            self.thread.start()
         except OSError:
             self.proc = None
         time.sleep(0.3)
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
-            time.sleep(0.15)
+            time.sleep(max(0.05, 2 * self.period))
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            self.thread.join(timeout=5)
 
     def summary(self) -> dict:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = (self.t1 if self.t1 is not None else time.time()) + self.period
+        window = [ln for ts, ln in self.samples if t0 <= ts <= t1]
+        if not window:  # region shorter than one period: the first sample after it started
+            window = [ln for ts, ln in self.samples if ts >= t0][:1]
         sm, mx, reasons = [], [], set()
-        for ln in getattr(self, "lines", []):
+        for ln in window:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 3 + len(REASON_FIELDS):
                 continue
@@ -282,46 +310,69 @@ def run_ours(args, wl: dict) -> None:
     plan = sk.GemmPlan(a, b, c, policy, tile, g)
     flops = 2.0 * m * n * k
     nbytes = 2.0 * (m * k + k * n) + 4.0 * m * n
-    # L2 flush between steps: write 256 MiB (> 126 MB L2), then read another 256 MiB so the
-    # lines left behind are clean (otherwise the GEMM pays the write-back of the flush's
-    # dirty lines).  Both run outside the per-step events.
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    scrub = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    sink = torch.empty(1, dtype=torch.float32, device="cuda")
-
-    def flush_l2():
-        flush.zero_()
-        torch.sum(scrub, dim=0, out=sink)
-
+    # Cold-L2 methodology: the timed steps rotate over R distinct operand sets (A, B, C)
+    # whose total exceeds 4x the 126 MB L2, so every step reads its operands from HBM
+    # (the set a step uses was last touched R-1 steps earlier, with >= 3 L2 capacities
+    # of other traffic since).  Steps run back to back on one stream (PDL lets each
+    # launch's prologue overlap the previous kernel's tail), bracketed by ONE pair of
+    # CUDA events, so per-step time is the steady-state launch-to-launch time.
+    set_bytes = 2 * (m * k + k * n) + 4 * m * n
+    n_sets = max(2, -(-ROTATE_BYTES // set_bytes))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1000 + rank)
+    plans = [plan]
+    for _ in range(n_sets - 1):
+        ar = torch.randn(m, k, generator=gen, device="cuda").to(in_dtype)
+        br = torch.randn(k, n, generator=gen, device="cuda").to(in_dtype)
+        cr = torch.empty(m, n, device="cuda", dtype=torch.float32)
+        plans.append(sk.GemmPlan(ar, br, cr, policy, tile, g))
     stream = torch.cuda.current_stream()
 
-    for _ in range(max(args.warmup, 3)):
-        flush_l2()
-        plan.launch()
+    for i in range(max(args.warmup, 3) + n_sets):
+        plans[i % n_sets].launch()
     torch.cuda.synchronize()
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(physical_gpu(local)) as clocks:
+        clocks.mark_start()
+        t_start.record(stream)
         for i in range(args.steps):
-            flush_l2()
-            starts[i].record(stream)
-            plan.launch()
-            ends[i].record(stream)
+            plans[i % n_sets].launch()
+        t_end.record(stream)
         torch.cuda.synchronize()
+        clocks.mark_end()
     if world > 1:
         torch.distributed.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
+    total_ms = t_start.elapsed_time(t_end)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     per_step_s = total_ms / args.steps / 1e3
     value = world * flops * args.steps / (total_ms / 1e3) / 1e12
+
+    # Isolated launches (informational): L2 flushed (256 MiB write + 256 MiB read, clean
+    # lines) before every launch, one event pair per launch.  Includes the ~6 us an
+    # event-timed EMPTY kernel costs after a flush on this GPU (tools/launchbench.cu).
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    scrub = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
+    iso = []
+    for _ in range(ISOLATED_STEPS):
+        flush.zero_()
+        torch.sum(scrub, dim=0, out=sink)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan.launch()
+        e1.record(stream)
+        iso.append((e0, e1))
+    torch.cuda.synchronize()
+    iso_us = statistics.median(e0.elapsed_time(e1) * 1e3 for e0, e1 in iso)
+    del flush, scrub
 
     # end to end through the public API with pinned host inputs
     e2e_steps = min(args.steps, args.e2e_steps)
@@ -374,7 +425,9 @@ def run_ours(args, wl: dict) -> None:
             "config": {
                 "workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]), "g": g,
                 "policy": policy.label, "out_dtype": "fp32",
-                "l2": "flushed before every step: 256 MiB write + 256 MiB read (clean lines), outside the per-step events",
+                "l2": f"cold: steps rotate over {n_sets} distinct operand sets "
+                      f"({n_sets * set_bytes / 2**20:.0f} MiB > 4x the 126 MB L2); no flush",
+                "timing": "one CUDA-event pair around K back-to-back launches on one stream",
                 "parallelism": f"replicas x{world} (GEMM is single-GPU)",
             },
             "pct_of_dense_peak": {
@@ -402,6 +455,12 @@ def run_ours(args, wl: dict) -> None:
                 "api": "paper_2408_11417_b200.execute_schedule(pinned host bf16 tensors)",
                 "steps": e2e_steps,
             },
+            "isolated_launch": {
+                "us_median": round(iso_us, 2), "tflops": round(flops / (iso_us * 1e-6) / 1e12, 2),
+                "steps": ISOLATED_STEPS,
+                "method": "L2 flushed before each launch, one event pair per launch (includes ~6 us "
+                          "event+launch floor of an empty kernel, tools/launchbench.cu)",
+            },
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),
         }
@@ -413,7 +472,7 @@ def run_ours(args, wl: dict) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")

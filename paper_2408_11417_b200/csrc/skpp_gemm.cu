@@ -19,10 +19,11 @@
 //       per warp) and TMA-stored to C; a partial item is written with
 //       coalesced stores to this CTA's workspace slot, whose flag is then
 //       released.  No CTA waits on another in phase 1.
-//     phase 2, after all items: for every split tile it touched, the CTA
-//       reduces ITS share of the tile's columns over ALL contributors' slots,
-//       pulled into the (now idle) operand ring with bulk copies, summed in
-//       increasing CTA order (fixed order => deterministic) and stored to C.
+//     phase 2, after all items (all 8 warps): a CTA reduces at most one
+//       split tile, a band of its rows over ALL contributors' slots, summed in
+//       a fixed order (peers in increasing CTA order, then the owner) so the
+//       result is deterministic, staged in shared memory and stored to C with
+//       coalesced row stores.
 //   Every CTA produces all its partials before it waits, so the wait graph
 //   is acyclic; flags carry an epoch kept in the workspace header, so the
 //   kernel is CUDA-graph replay safe.
@@ -351,6 +352,8 @@ enum : int {
   TL_EPI_FIRST = 8,   // epilogue saw its first accumulator
   TL_PART_ISSUED = 9, // first partial: all TMA stores issued
   TL_PART_FLAG = 10,  // first partial: flag released
+  TL_SUM1 = 11,       // phase 2: first summation pass done (thread 128)
+  TL_SUM2 = 12,       // phase 2: owner pass done (only when the owner was late)
   TL_EVENTS = 16
 };
 __device__ __forceinline__ uint64_t gtimer() {
@@ -440,71 +443,104 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t epoch) 
   }
 }
 
-// Phase 2(a): part[(j - j0)*128 + r] = sum over peers t = 1..nc-1 (in order) of
-// slot(x0+t)[j][r] for this thread's column groups j = ga, ga+2, ... < j1.
-template <int G, int KB, int CG>
-__device__ __forceinline__ void sum_peers(const ReduceArgs& ra, const float4* base_r, uint32_t ga,
-                                          uint32_t j0, uint32_t j1, float4* part, uint32_t r) {
-  for (uint32_t jb = ga; jb < j1; jb += 2 * G) {
+// Phase 2 works on a BAND of rows of the split tile: reducer idx of nr owns rows
+// [R0, R0 + nrows) of its row half and every column.  Element e of the band is
+// column group j = e / nrows, band row ro = e % nrows, i.e. float4 (j*128 + R0 + ro)
+// of every slot, so consecutive threads read consecutive rows of one column group
+// (coalesced; slots are column-group major).  Terms are added in the fixed order
+// peer x0+1, ..., peer x0+nc-1, owner x0 (term index i < nc-1 is peer x0+1+i,
+// term nc-1 is x0), starting from +0, so the bits never depend on timing or on
+// whether the owner term was added in the same pass.  The band is accumulated
+// in shared memory (stage[ro][j], row stride V+1 float4) and stored to C row by
+// row (coalesced) by band_store.
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void st_shared_f4(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// Scalars passed by value: a noinline callee keeps them in registers.
+template <int G, int KB>
+__device__ __noinline__ void band_sum(const float4* __restrict__ wsv, uint64_t slot_v, uint64_t peer_slot0,
+                                      uint32_t peer_slot_step, uint64_t owner_slot, uint32_t nc,
+                                      uint32_t R0, uint32_t nrows, uint32_t V, uint32_t term_begin,
+                                      uint32_t term_end, uint32_t accumulate, uint32_t stage,
+                                      uint32_t ft) {
+  const uint32_t total = nrows * V;
+  for (uint32_t e0 = ft; e0 < total; e0 += G * kThreads) {
     float4 acc[G];
+    uint32_t off[G];
+    uint32_t saddr[G];
 #pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t t0 = 1; t0 < ra.nc; t0 += KB) {
+    for (int g = 0; g < G; ++g) {
+      const uint32_t e = e0 + g * kThreads;
+      const uint32_t j = e / nrows, ro = e - j * nrows;
+      off[g] = j * kBM + R0 + ro;
+      saddr[g] = stage + (ro * (V + 1) + j) * 16;
+      acc[g] = (accumulate && e < total) ? ld_shared_f4(saddr[g]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (uint32_t t0 = term_begin; t0 < term_end; t0 += KB) {
       float4 q[G][KB];
 #pragma unroll
       for (int b = 0; b < KB; ++b) {
-        if (t0 + b < ra.nc) {
-          const float4* src = base_r + 2 * ((ra.x0 + t0 + b) * CG + ra.rank) * ra.slot_v;
+        if (t0 + b < term_end) {
+          const uint64_t slot = (t0 + b < nc - 1) ? peer_slot0 + (uint64_t)(t0 + b) * peer_slot_step : owner_slot;
+          const float4* src = wsv + slot * slot_v;
 #pragma unroll
           for (int g = 0; g < G; ++g)
-            if (jb + 2 * g < j1) q[g][b] = ld_cg_f4(src + (uint64_t)(jb + 2 * g) * kBM);
+            if (e0 + g * kThreads < total) q[g][b] = ld_cg_f4(src + off[g]);
         }
       }
 #pragma unroll
       for (int b = 0; b < KB; ++b) {
-        if (t0 + b < ra.nc) {
+        if (t0 + b < term_end) {
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            if (jb + 2 * g < j1) {
-              acc[g].x += q[g][b].x;
-              acc[g].y += q[g][b].y;
-              acc[g].z += q[g][b].z;
-              acc[g].w += q[g][b].w;
-            }
+            acc[g].x += q[g][b].x;
+            acc[g].y += q[g][b].y;
+            acc[g].z += q[g][b].z;
+            acc[g].w += q[g][b].w;
           }
         }
       }
     }
 #pragma unroll
     for (int g = 0; g < G; ++g)
-      if (jb + 2 * g < j1) part[(jb + 2 * g - j0) * kBM + r] = acc[g];
+      if (e0 + g * kThreads < total) st_shared_f4(saddr[g], acc[g]);
   }
 }
 
-// Phase 2(b): C[row][j] = part + slot(x0)[j][r], 8 loads of x0's slot in flight.
-__device__ __forceinline__ void add_owner_and_store(const GemmParams& p, const ReduceArgs& ra,
-                                                    const float4* base_r, uint32_t ga, uint32_t j0,
-                                                    uint32_t j1, const float4* part, uint32_t r,
-                                                    uint64_t grow, uint64_t gcol0) {
-  constexpr int NB = 8;
-  const float4* src = base_r + ra.slot0 * ra.slot_v;
-  for (uint32_t jb = ga; jb < j1; jb += 2 * NB) {
-    float4 q[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i)
-      if (jb + 2 * i < j1) q[i] = ld_cg_f4(src + (uint64_t)(jb + 2 * i) * kBM);
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      if (jb + 2 * i < j1) {
-        float4 a = part[(jb + 2 * i - j0) * kBM + r];
-        a.x += q[i].x;
-        a.y += q[i].y;
-        a.z += q[i].z;
-        a.w += q[i].w;
-        store_vec4(p, grow, gcol0 + 4 * (jb + 2 * i), a);
-      }
-    }
+// Store the reduced band: consecutive threads take consecutive column groups of
+// one row, so a warp writes 512 contiguous bytes of C (fp32) per instruction.
+__device__ __forceinline__ void band_store(const GemmParams& p, uint32_t stage, uint32_t nrows,
+                                           uint32_t V, uint64_t row0, uint64_t col0, uint32_t ft) {
+  const uint32_t total = nrows * V;
+  for (uint32_t e = ft; e < total; e += kThreads) {
+    const uint32_t ro = e / V, j = e - ro * V;
+    store_vec4(p, row0 + ro, col0 + 4 * j, ld_shared_f4(stage + (ro * (V + 1) + j) * 16));
   }
+}
+
+// Term i < nc-1 is peer x0+1+i (its first Stream-K item: slot 2*cta, cta =
+// (x0+1+i)*CG + rank); term nc-1 is the owner x0 (slot0).  Register-staged
+// loads, <= 24 float4 in flight per thread: larger variants spill, and a
+// cp.async variant (all terms' bands in flight through the idle ring) measured
+// 3-20% slower on every fixup-heavy shape tried (tools/ab_reduce.py).
+template <int CG>
+__device__ __forceinline__ void band_reduce(const ReduceArgs& ra, uint32_t R0, uint32_t nrows, uint32_t V,
+                                            uint32_t term_begin, uint32_t term_end, bool accumulate,
+                                            uint32_t stage, uint32_t ft) {
+  const uint64_t peer0 = 2 * ((ra.x0 + 1) * CG + ra.rank);
+  if (ra.nc <= 4)
+    band_sum<4, 4>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, term_begin, term_end,
+                   accumulate, stage, ft);
+  else
+    band_sum<2, 12>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, term_begin, term_end,
+                    accumulate, stage, ft);
 }
 
 // Hand an accumulator stage back to the MMA issuer (the rank-0 CTA's barrier).
@@ -819,22 +855,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   // contributors whose first Stream-K item lies in u: x0 (only if its range
   // starts exactly at the tile) .. x1, so every CTA reduces at most one tile
   // and every split tile has at least one reducer (x1).  Reducer idx of nr
-  // sums column groups [idx*V/nr, (idx+1)*V/nr) of its row half over ALL nc
-  // contributors' slots, in increasing CTA order.  Thread ft owns row (ft & 127) and, per pass of four
-  // column groups, groups jb + (ft >> 7) and jb + (ft >> 7) + 2.  Loads are
-  // coalesced (a warp reads 32 consecutive rows of one group = 512 B) and kept
-  // 16 deep per thread (64 KiB per CTA) because this step is bound by L2
-  // latency x bytes in flight, not by bandwidth.
+  // owns the row band [idx*128/nr, (idx+1)*128/nr) of its row half and sums it
+  // over ALL nc contributors' slots in a fixed order (band_sum).  One pass
+  // when the owner x0 has published by the time the peers have (every
+  // contributor ends its mainloop together); otherwise the peers are summed
+  // first and x0 — whose item may be its LAST — is added when it lands.
   __syncwarp();          // producer / MMA lanes rejoin their warps
   phase2_bar_sync();     // split tiles published by the epilogue
   if (s.sk_tiles) {
     const uint32_t ft = threadIdx.x;
-    const uint32_t r = ft & 127, h = ft >> 7;
     const uint32_t n_split = nsplit_smem[0];
     const uint32_t epoch = ld_relaxed_gpu(p.hdr) + 1u;
     constexpr uint32_t V = BN / 4;  // float4 column groups per tile row
+    static_assert(C::RING_BYTES >= (uint32_t)kBM * (V + 1) * 16, "phase-2 band stage");
     const float4* wsv = reinterpret_cast<const float4*>(p.ws);
     const uint64_t slot_v = (uint64_t)kBM * V;  // float4 per slot
+    volatile uint32_t* peers_seen = nsplit_smem + 2;
     for (uint32_t si = 0; si < n_split; ++si) {
       const uint64_t u = split_smem[si];
       const uint64_t x0 = (u * s.ipt) / s.ipw;
@@ -844,34 +880,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t r_lo = x0 + (aligned ? 0 : 1);
       const uint32_t nr = (uint32_t)(x1 - r_lo + 1);
       const uint32_t idx = (uint32_t)(x - r_lo);
-      const uint32_t j0 = (uint32_t)(((uint64_t)idx * V) / nr);
-      const uint32_t j1 = (uint32_t)(((uint64_t)(idx + 1) * V) / nr);
-      if (j0 == j1) continue;
+      const uint32_t R0 = (uint32_t)(((uint64_t)idx * kBM) / nr);
+      const uint32_t R1 = (uint32_t)(((uint64_t)(idx + 1) * kBM) / nr);
+      if (R0 == R1) continue;
       // contributor x0+t wrote its first Stream-K item (slot 2*cta), except x0
       // when its range starts inside an earlier tile (tile u is its last item)
       const uint64_t slot0 = 2 * (x0 * CG + rank) + (aligned ? 0 : 1);
       const uint64_t tile = s.dp_tiles + u;
-      const uint64_t grow = (tile / s.n_tiles) * TILE_M + rank * kBM + r;
+      const uint64_t row0 = (tile / s.n_tiles) * TILE_M + rank * kBM + R0;
       const uint64_t gcol0 = (tile % s.n_tiles) * BN;
       const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc};
-      const float4* base_r = wsv + r;  // this thread's row in every slot
-      float4* part = reinterpret_cast<float4*>(smem);  // idle operand ring: [group - j0][row]
-      // (a) the peers x0+1 .. x1 produce this tile as their FIRST item and are
-      //     ready early: sum them (in increasing CTA order) into shared memory
-      //     while x0, whose item may be its LAST, is still running.
-      for (uint32_t t = 1 + ft; t < nc; t += kThreads) wait_flag(p.flags + 2 * ((x0 + t) * CG + rank), epoch);
+      const uint32_t stage = smem_u32(smem);  // idle operand ring: float4 [row][V+1]
+      // Peer flags are awaited by one thread each; thread kThreads-1 polls the
+      // owner's flag until either it is up or every peer has been seen.
+      if (ft == 0) *peers_seen = 0u;
+      phase2_bar_sync();
+      if (ft < kThreads - 1) {
+        for (uint32_t t = 1 + ft; t < nc; t += kThreads - 1) {
+          wait_flag(p.flags + 2 * ((x0 + t) * CG + rank), epoch);
+          atomicAdd(const_cast<uint32_t*>(peers_seen), 1u);
+        }
+      }
+      if (ft == kThreads - 1) {
+        const uint32_t want = nc - 1;
+        uint32_t ready = 0;
+        const long long t0 = clock64();
+        while (true) {
+          if (ld_acquire_gpu(p.flags + slot0) == epoch) { ready = 1; break; }
+          if (*peers_seen >= want) break;
+          watchdog(t0, 6);
+        }
+        nsplit_smem[1] = ready;
+      }
       phase2_bar_sync();
       if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
-      if (nc <= 4)
-        sum_peers<4, 3, CG>(ra, base_r, j0 + h, j0, j1, part, r);
-      else if (nc <= 7)
-        sum_peers<2, 6, CG>(ra, base_r, j0 + h, j0, j1, part, r);
-      else
-        sum_peers<1, 12, CG>(ra, base_r, j0 + h, j0, j1, part, r);
-      // (b) x0 last: fixed order (peers, then x0) => deterministic.
-      if (ft == 0) wait_flag(p.flags + slot0, epoch);
+      const bool owner_ready = nsplit_smem[1] != 0;
+      const uint32_t nrows = R1 - R0;
+      band_reduce<CG>(ra, R0, nrows, V, 0, owner_ready ? nc : nc - 1, false, stage, ft);
+      if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM1);
+      if (!owner_ready) {
+        if (ft == 0) wait_flag(p.flags + slot0, epoch);
+        phase2_bar_sync();  // also orders the stage writes above before the re-reads below
+        band_reduce<CG>(ra, R0, nrows, V, nc - 1, nc, true, stage, ft);
+        if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM2);
+      }
       phase2_bar_sync();
-      add_owner_and_store(p, ra, base_r, j0 + h, j0, j1, part, r, grow, gcol0);
+      band_store(p, stage, nrows, V, row0, gcol0, ft);
+      phase2_bar_sync();  // stage and nsplit_smem[1..2] are reused by the next split tile
     }
     if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
     // ---- launch epilogue: the last CTA out advances the workspace epoch

@@ -103,6 +103,29 @@ __global__ void bulk_kernel(const char* src, size_t bytes_per_cta, uint32_t chun
   }
 }
 
+// Each CTA writes its contiguous share from shared memory with bulk S2G copies of
+// `chunk` bytes, `inflight` bulk groups outstanding.
+__global__ void bulk_store_kernel(char* dst, size_t bytes_per_cta, uint32_t chunk, uint32_t inflight,
+                                  int reps) {
+  extern __shared__ __align__(1024) char sm[];
+  if (threadIdx.x != 0) return;
+  char* base = dst + (size_t)blockIdx.x * bytes_per_cta;
+  const size_t n_chunks = bytes_per_cta / chunk;
+  for (int r = 0; r < reps; ++r) {
+    for (size_t c = 0; c < n_chunks; ++c) {
+      const uint32_t slot = c % inflight;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(base + c * chunk),
+                   "r"(smem_u32(sm + slot * chunk)), "r"(chunk)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (inflight == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      else if (inflight == 4) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory");
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <typename F>
 static float best_ms(F launch) {
   cudaEvent_t a, b;
@@ -164,6 +187,31 @@ int main() {
         }
       }
     }
+  }
+  CK(cudaFuncSetAttribute(bulk_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  for (size_t sz : {small, big}) {
+    for (uint32_t chunk : {4096u, 16384u, 32768u}) {
+      for (uint32_t inflight : {2u, 4u, 8u}) {
+        if ((size_t)chunk * inflight > 196608) continue;
+        for (int grid : {sms, 1}) {
+          const size_t per_cta = grid == 1 ? (size_t)(8 << 20) : (sz / sms) / chunk * chunk;
+          const int reps = (sz == small && grid != 1) ? 10 : 1;
+          float ms = best_ms([&] {
+            bulk_store_kernel<<<grid, 32, chunk * inflight>>>(buf, per_cta, chunk, inflight, reps);
+          });
+          printf("bulkst %5s chunk %6u inflight %2u grid %4d: %8.1f GB/s (%.1f per CTA)\n",
+                 sz == small ? "L2" : "DRAM", chunk, inflight, grid, per_cta * grid * reps / ms / 1e6,
+                 per_cta * reps / ms / 1e6);
+        }
+      }
+    }
+  }
+  for (int grid : {sms, 1}) {
+    const size_t n = grid == 1 ? (size_t)(8 << 20) / 16 : small / 16;
+    const int r = grid == 1 ? 1 : 20;
+    float ms = best_ms([&] { stg_kernel<8><<<grid, 1024>>>((float4*)buf, n, r); });
+    printf("stg1024 L2 grid %4d: %8.1f GB/s (%.1f GB/s per CTA)\n", grid, n * 16.0 * r / ms / 1e6,
+           n * 16.0 * r / ms / 1e6 / grid);
   }
   CK(cudaGetLastError());
   return 0;

@@ -9,7 +9,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-EVENTS = ["start", "first_tma", "first_full", "mma_done", "phase1", "waited", "phase2", "-", "epi_first", "part_issued", "part_flag"]
+EVENTS = ["start", "first_tma", "first_full", "mma_done", "phase1", "waited", "phase2", "-", "epi_first", "part_issued", "part_flag", "sum1", "sum2"]
 
 
 def main() -> None:
@@ -57,7 +57,7 @@ def main() -> None:
     base = t[:, 0][t[:, 0] > 0].min()
     print(f"{args.m}x{args.n}x{args.k} {args.policy} tile {args.tile} flush={args.flush}: "
           f"event time {e0.elapsed_time(e1) * 1e3:.1f} us, "
-          f"kernel span {(t[:, :11].max() - base) / 1e3:.2f} us")
+          f"kernel span {(t[:, :13].max() - base) / 1e3:.2f} us")
     for i, name in enumerate(EVENTS):
         if name == "-":
             continue
