@@ -100,7 +100,8 @@ int skpp_validate_intervals(const uint64_t* starts, const uint64_t* ends, uint64
 
 /* Bytes of fp32 partial workspace + flags that skpp_gemm_launch needs. */
 uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_tile_t* t, uint32_t g);
-/* Tile shapes the sm_100a kernel implements: blk_m == 128, blk_n in {64,128,256}, blk_k in {16,32,64}. */
+/* Tile shapes the sm_100a kernel implements: blk_m == 128 with blk_n in {64,128,256}, blk_k in
+   {16,32,64,128}; blk_m == 256 (CTA pair) with blk_n in {128,256}, blk_k in {32,64,128}. */
 int skpp_tile_supported(const skpp_tile_t* t);
 /* Persistent Stream-K++ GEMM C = A @ B on the current device, stream-ordered.
    The workspace must be zero-filled the first time it is used; afterwards the

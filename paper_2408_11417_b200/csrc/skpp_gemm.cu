@@ -308,15 +308,18 @@ struct Cfg {
   static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 48 + 1023) / 1024 * 1024;
   static constexpr uint32_t SMEM = RING_BYTES + kStagingBytes + BAR_BYTES + 1024;
   // A: K-major, one swizzle atom along K (BK*2 bytes = 32/64/128 B)
-  static constexpr uint32_t A_LAYOUT = BK == 64 ? 2u : (BK == 32 ? 4u : 6u);
-  static constexpr uint32_t A_SBO = 8 * BK * 2;  // 8 rows of one atom
+  // BK = 128: two SW128 sub-tiles of [128 rows][64 k] (one TMA box each, 16 KiB apart)
+  static constexpr uint32_t A_LAYOUT = BK >= 64 ? 2u : (BK == 32 ? 4u : 6u);
+  static constexpr uint32_t A_SBO = BK >= 64 ? 1024u : 8 * BK * 2;  // 8 rows of one atom
+  static constexpr uint32_t A_OPS = BK > 64 ? BK / 64 : 1;          // TMA boxes per stage
+  static constexpr uint32_t A_SUB = A_BYTES / A_OPS;                // bytes per A sub-tile
   // B: N-major SW128, 64-column chunks of BK rows x 128 B
   static constexpr uint32_t B_LAYOUT = 2u;
   static constexpr uint32_t B_LBO = BK * 128;  // next 64-wide N chunk
   static constexpr uint32_t B_SBO = 1024;      // next 8 K-rows
   static_assert(BN % 64 == 0 && BN <= 256 && BNC % 64 == 0, "BN");
   static_assert(CG == 1 || CG == 2, "CG");
-  static_assert(BK == 16 || BK == 32 || BK == 64, "BK");
+  static_assert(BK == 16 || BK == 32 || BK == 64 || BK == 128, "BK");
   static_assert(STAGES >= 2, "stages");
   static_assert(SMEM <= 232448, "shared memory");
 };
@@ -657,7 +660,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t k0 = (int32_t)(kk * BK);
         if constexpr (CG == 1) {
           if (load_a) {
-            tma_load_2d(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
+#pragma unroll
+            for (uint32_t j = 0; j < C::A_OPS; ++j)
+              tma_load_2d(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
           } else if (p.b3d) {  // all of the stage's B columns in one 3-D box
             tma_load_3d(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
           } else {
@@ -668,7 +673,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           if (load_a) {
-            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, k0, m0, &full_bar[stage]);
+#pragma unroll
+            for (uint32_t j = 0; j < C::A_OPS; ++j)
+              tma_load_2d_pair(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
           } else if (p.b3d) {
             tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
           } else {
@@ -706,7 +713,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = umma_desc(a_addr + k * 32, 0, C::A_SBO, C::A_LAYOUT);
+            // k-step k covers elements [16k, 16k+16): sub-tile 16k/64, 32 B per step inside it
+            const uint64_t ad = umma_desc(a_addr + (k * 16 / 64) * C::A_SUB + (k * 16 % 64) * 2, 0,
+                                          C::A_SBO, C::A_LAYOUT);
             const uint64_t bd = umma_desc(b_addr + k * 2048, C::B_LBO, C::B_SBO, C::B_LAYOUT);
             if constexpr (CG == 1)
               umma_f16(dtm, ad, bd, p.idesc, (kk > it.kb || k > 0) ? 1u : 0u);
@@ -1134,8 +1143,13 @@ static int dispatch_tile(const skpp_tile_t* t, F&& f) {
   using I64 = std::integral_constant<int, 64>;
   using I128 = std::integral_constant<int, 128>;
   using I256 = std::integral_constant<int, 256>;
+  using I128k = std::integral_constant<int, 128>;
   if (t->blk_m == (uint32_t)kBM) {
-    if (t->blk_k == 64) {
+    if (t->blk_k == 128) {
+      if (t->blk_n == 64) return f(I64{}, I128k{}, I1{});
+      if (t->blk_n == 128) return f(I128{}, I128k{}, I1{});
+      if (t->blk_n == 256) return f(I256{}, I128k{}, I1{});
+    } else if (t->blk_k == 64) {
       if (t->blk_n == 64) return f(I64{}, I64{}, I1{});
       if (t->blk_n == 128) return f(I128{}, I64{}, I1{});
       if (t->blk_n == 256) return f(I256{}, I64{}, I1{});
@@ -1149,7 +1163,10 @@ static int dispatch_tile(const skpp_tile_t* t, F&& f) {
       if (t->blk_n == 256) return f(I256{}, I16{}, I1{});
     }
   } else if (t->blk_m == 2u * kBM) {
-    if (t->blk_k == 64) {
+    if (t->blk_k == 128) {
+      if (t->blk_n == 128) return f(I128{}, I128k{}, I2{});
+      if (t->blk_n == 256) return f(I256{}, I128k{}, I2{});
+    } else if (t->blk_k == 64) {
       if (t->blk_n == 128) return f(I128{}, I64{}, I2{});
       if (t->blk_n == 256) return f(I256{}, I64{}, I2{});
     } else if (t->blk_k == 32) {
@@ -1258,7 +1275,7 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
     set_error("tile shape " + std::to_string(t->blk_m) + "x" + std::to_string(t->blk_n) + "x" +
               std::to_string(t->blk_k) +
               " is not implemented by the sm_100a kernel (blk_m=128, blk_n in {64,128,256}, "
-              "blk_k in {16,32,64})");
+              "blk_k in {16,32,64,128}; blk_m=256: blk_n in {128,256}, blk_k in {32,64,128})");
     return SKPP_ETILE;
   }
   if (ops->in_dtype != SKPP_F16 && ops->in_dtype != SKPP_BF16) {
@@ -1322,11 +1339,11 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   pl->block_n = t->blk_n;
   pl->cg = t->blk_m / kBM;
   const uint32_t BK = t->blk_k;
-  const CUtensorMapSwizzle aswz = BK == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+  const CUtensorMapSwizzle aswz = BK >= 64   ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : BK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                              : CU_TENSOR_MAP_SWIZZLE_32B;
   const CUtensorMapDataType in_dt = map_dtype(ops->in_dtype);
-  rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK, kBM, aswz);
+  rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK > 64 ? 64 : BK, kBM, aswz);
   const uint32_t bnc = t->blk_n / (t->blk_m / kBM);  // B columns per CTA
   const bool b3d = g_b3d && p->n % 64 == 0 && bnc > 64;
   if (!rc && b3d) {

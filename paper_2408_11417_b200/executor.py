@@ -192,8 +192,8 @@ class GemmPlan:
         if not tile_supported(tile):
             raise ValueError(
                 f"tile {tile.blk_m}x{tile.blk_n}x{tile.blk_k} is not implemented by the sm_100a "
-                "kernel (blk_m=128: blk_n in {64,128,256}, blk_k in {16,32,64}; "
-                "blk_m=256 CTA pair: blk_n in {128,256}, blk_k in {32,64})"
+                "kernel (blk_m=128: blk_n in {64,128,256}, blk_k in {16,32,64,128}; "
+                "blk_m=256 CTA pair: blk_n in {128,256}, blk_k in {32,64,128})"
             )
         m, k = a.shape
         n = b.shape[1]

@@ -151,6 +151,49 @@ def measure_size(
     return rank_costs(size, costs)
 
 
+def measure_size_tiles(
+    size: ProblemSize,
+    tiles: list[TileShape],
+    policies: list[Policy],
+    params: MeasureParams,
+    pool: OperandPool,
+    rounds: int = 5,
+) -> list[tuple[TileShape, TuneRecord]]:
+    """Time every (tile, policy) of one size with the distinct schedules measured
+    round-robin (``rounds`` passes, rotated start, median per schedule), so clock
+    drift under the power cap during the measurement does not favour whichever
+    tile happened to run first."""
+    a, b, c = pool.views(size)
+    keys: dict[tuple, GemmPlan] = {}
+    cfg_key = []
+    for ti, tile in enumerate(tiles):
+        g = default_g(tile)
+        for pol in policies:
+            plan = GemmPlan(a, b, c, pol, tile, g)
+            key = (ti, schedule_signature(plan.sched_c))
+            keys.setdefault(key, plan)
+            cfg_key.append((ti, pol, key))
+    order = list(keys)
+    samples: dict[tuple, list[float]] = {k: [] for k in order}
+    for r in range(rounds):
+        for i in range(len(order)):
+            key = order[(i + r) % len(order)]
+            samples[key].append(time_plan(keys[key], params))
+    out = []
+    for ti, tile in enumerate(tiles):
+        costs = []
+        for tj, pol, key in cfg_key:
+            if tj != ti:
+                continue
+            us = sorted(samples[key])[len(samples[key]) // 2]
+            tflops = size.flops / (us * 1e-6) / 1e12
+            partial, full, _ = count_partials(keys[key].sched_c)
+            costs.append((pol, CostEstimate(makespan=us, utilization=tflops / params.peak_tflops,
+                                            atomic_writes=partial, full_stores=full)))
+        out.append((tile, rank_costs(size, costs)))
+    return out
+
+
 def tune_sizes(
     sizes: list[ProblemSize],
     tile: TileShape,

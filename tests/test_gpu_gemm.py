@@ -60,6 +60,10 @@ def _policies():
         (384, 640, 1088, 256, 64),
         (200, 136, 520, 64, 32),      # ragged M/N/K, BK=32
         (130, 72, 48, 64, 16),        # ragged, BK=16
+        (512, 512, 4096, 128, 128),   # BK=128: two A boxes per stage
+        (1024, 1024, 1024, 256, 128),
+        (200, 136, 520, 64, 128),     # ragged, K tail inside the second A box
+        (136, 264, 72, 128, 128),     # K < BK: second A box entirely out of bounds
     ],
 )
 def test_integer_inputs_bitwise_every_policy(m, n, k, blk_n, blk_k):
@@ -74,6 +78,8 @@ def test_integer_inputs_bitwise_every_policy(m, n, k, blk_n, blk_k):
         (512, 512, 8192, 128, 64),    # fixup-heavy
         (600, 392, 1000, 256, 64),    # ragged: half-empty second CTA rows / columns
         (300, 200, 520, 128, 32),
+        (512, 512, 8192, 256, 128),   # BK=128 pair
+        (600, 392, 1000, 128, 128),
     ],
 )
 def test_cta_pair_tiles_bitwise_every_policy(m, n, k, blk_n, blk_k):

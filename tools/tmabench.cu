@@ -1,8 +1,10 @@
-// tmabench.cu — per-SM TMA tensor-load throughput vs operations per stage.
+// tmabench.cu — per-SM TMA tensor-load throughput vs bytes per op and ops per stage.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tmabench tools/tmabench.cu && ./tmabench
-// A ring of S stages of 32 KiB; each stage is filled by OPS tensor loads (3-D box
-// {64 bf16, 64 rows, 4/OPS chunks}) from an L2-resident 64 MiB tensor; a consumer
-// thread releases stages as they land.  Reports GB/s per CTA for 1 and 148 CTAs.
+// One thread per CTA keeps a ring of S stages in flight; each stage of STAGE bytes
+// is filled by OPS tensor loads of 3-D boxes {64 bf16, 64 rows, chunks} (8 KiB per
+// chunk, SWIZZLE_128B) from an L2-resident 64 MiB tensor and released as it lands.
+// Reports GB/s per CTA and ns per stage for 1 and 148 CTAs: if the time per stage
+// stays flat as STAGE grows, the TMA op (not bytes) is the per-SM limit.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -23,16 +25,16 @@ __device__ __forceinline__ void wait_bar(uint64_t* b, uint32_t ph) {
         : "r"(smem_u32(b)), "r"(ph));
 }
 
-template <int OPS>
-__global__ void ring_kernel(const __grid_constant__ CUtensorMap tm, int iters, int stages, int rows) {
+__global__ void ring_kernel(const __grid_constant__ CUtensorMap tm, int iters, int stages, int stage_bytes,
+                            int ops, int rows) {
   extern __shared__ __align__(1024) char sm[];
   __shared__ __align__(8) uint64_t full[16];
   if (threadIdx.x != 0) return;
   for (int i = 0; i < stages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  constexpr int CH = 4 / OPS;  // chunks per op
+  const int op_bytes = stage_bytes / ops;
+  const int ch = op_bytes / 8192;  // chunks per op
   uint32_t phase[16] = {0};
-  const int rows_total = rows;
   for (int it = 0; it < iters + stages; ++it) {
     const int s = it % stages;
     if (it >= stages) {
@@ -40,14 +42,15 @@ __global__ void ring_kernel(const __grid_constant__ CUtensorMap tm, int iters, i
       phase[s] ^= 1;
     }
     if (it < iters) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(32768)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                   "r"(stage_bytes)
                    : "memory");
-      const int row = ((blockIdx.x * 37 + it) * 64) % rows_total;
-      for (int o = 0; o < OPS; ++o) {
+      const int row = ((blockIdx.x * 37 + it) * 64) % rows;
+      for (int o = 0; o < ops; ++o) {
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(sm + s * 32768 + o * (32768 / OPS))),
-            "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(row), "r"(((blockIdx.x + it) % 4) * 4 + o * CH),
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(sm + s * stage_bytes + o * op_bytes)),
+            "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(row), "r"(o * ch),
             "r"(smem_u32(&full[s]))
             : "memory");
       }
@@ -60,54 +63,54 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q);
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fnp);
-  // tensor: [chunks=16][rows=4096][64 bf16] (128 B rows) = 8 MiB, x8 copies region = L2 resident
+  // tensor [16 chunks][rows][64 bf16]: rows of 128 B, chunk stride = rows*128 (64 MiB, L2 resident)
   void* buf;
   cudaMalloc(&buf, 64ull << 20);
   cudaMemset(buf, 0, 64ull << 20);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  for (int row_stride : {128, 1024, 8192, 32768})
-  for (int ops : {1, 2, 4}) {
-    if (row_stride != 128 && ops != 2) continue;
-    CUtensorMap tm;
-    const int ch = 4 / ops;
-    // rows of 128 B at `row_stride`; 16 "chunks" of 64 columns side by side in a row
-    // when row_stride >= 2 KiB, else stacked (contiguous case)
-    const int rows = row_stride >= 2048 ? (int)((64ull << 20) / row_stride) : 4096;
-    cuuint64_t dims[3] = {64, (cuuint64_t)rows, 16};
-    cuuint64_t strides[2] = {(cuuint64_t)row_stride, row_stride >= 2048 ? 128ull : 128ull * 4096};
-    cuuint32_t box[3] = {64, 64, (cuuint32_t)ch};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      printf("encode failed %d\n", (int)r);
-      return 1;
-    }
-    for (int stages : {4, 6}) {
-      for (int grid : {1, sms}) {
-        const int iters = 2000;
-        const size_t smem = 32768 * stages;
-        void (*k)(CUtensorMap, int, int, int) = ops == 1 ? ring_kernel<1> : ops == 2 ? ring_kernel<2> : ring_kernel<4>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaEvent_t a, b;
-        cudaEventCreate(&a);
-        cudaEventCreate(&b);
-        float best = 1e30f;
-        for (int rep = 0; rep < 4; ++rep) {
-          cudaEventRecord(a);
-          k<<<grid, 32, smem>>>(tm, iters, stages, rows - 64);
-          cudaEventRecord(b);
-          cudaEventSynchronize(b);
-          float ms;
-          cudaEventElapsedTime(&ms, a, b);
-          if (rep && ms < best) best = ms;
+  const int rows = 32768;  // 16 chunks x 32768 rows x 128 B = 64 MiB
+  for (int stage_bytes : {16384, 32768, 65536}) {
+    for (int ops : {1, 2, 4}) {
+      const int ch = stage_bytes / ops / 8192;
+      if (ch < 1) continue;
+      CUtensorMap tm;
+      cuuint64_t dims[3] = {64, (cuuint64_t)rows, 16};
+      cuuint64_t strides[2] = {128, 128ull * rows};
+      cuuint32_t box[3] = {64, 64, (cuuint32_t)ch};
+      cuuint32_t es[3] = {1, 1, 1};
+      CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        printf("encode failed %d\n", (int)r);
+        return 1;
+      }
+      for (int stages : {3, 6}) {
+        if (stages * stage_bytes > 200 * 1024) continue;
+        for (int grid : {1, sms}) {
+          const int iters = 3000;
+          const size_t smem = (size_t)stage_bytes * stages;
+          cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          cudaEvent_t a, b;
+          cudaEventCreate(&a);
+          cudaEventCreate(&b);
+          float best = 1e30f;
+          for (int rep = 0; rep < 4; ++rep) {
+            cudaEventRecord(a);
+            ring_kernel<<<grid, 32, smem>>>(tm, iters, stages, stage_bytes, ops, rows - 64);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep && ms < best) best = ms;
+          }
+          cudaError_t e = cudaGetLastError();
+          printf("stage %6d B ops %d (op %6d B) stages %d grid %3d: %7.1f GB/s per CTA %8.1f GB/s total  %6.1f ns/stage %s\n",
+                 stage_bytes, ops, stage_bytes / ops, stages, grid, (double)stage_bytes * iters / best / 1e6,
+                 (double)stage_bytes * iters * grid / best / 1e6, best * 1e6 / iters,
+                 e == cudaSuccess ? "" : cudaGetErrorString(e));
         }
-        cudaError_t e = cudaGetLastError();
-        printf("row_stride %6d ops/stage %d (box %5d B) stages %d grid %3d: %7.1f GB/s per CTA, %8.1f GB/s total  %s\n", ops,
-               row_stride, 32768 / ops, stages, grid, 32768.0 * iters / best / 1e6, 32768.0 * iters * grid / best / 1e6,
-               e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
     }
   }
