@@ -335,7 +335,7 @@ struct GemmParams {
   uint32_t c_tma;      // C tensor map valid: phase-1 FULL tiles use TMA stores
   float* ws;           // 2g partial slots of BM x BN fp32, row-major
   uint32_t* flags;     // 2g slot flags (== epoch when the slot holds this launch's partial)
-  uint32_t* hdr;       // [0] epoch of the last completed launch, [1] CTAs done in this launch
+  uint32_t* hdr;       // [0] epoch of the last completed launch, [1] CTAs of this launch that read [0]
   int64_t* trace;
   uint64_t trace_cap;
   int64_t* trace_counts;
@@ -747,7 +747,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = (et == 0);
     const uint32_t cta = blockIdx.x;  // workspace slots are per CTA (per row half)
     const bool out16 = p.out_dtype != SKPP_F32;
-    const uint32_t epoch = s.sk_tiles ? (ld_relaxed_gpu(p.hdr) + 1u) : 0u;
+    // Launch epoch (Stream-K launches only): every CTA reads the epoch of the last
+    // completed launch and arrives on a counter; the LAST arrival — after every
+    // CTA has read it — advances the header for the next launch and resets the
+    // counter.  All of it happens here, at the start, hidden behind the mainloop;
+    // the next launch reads the header only after griddepcontrol.wait, i.e. after
+    // this grid completed.  The leader alone publishes flags; phase 2 gets the
+    // epoch through shared memory.
+    uint32_t epoch = 0;
+    if (s.sk_tiles && leader) {
+      epoch = ld_relaxed_gpu(p.hdr) + 1u;
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the read above precedes the arrival
+      if (atomicAdd(p.hdr + 1, 1u) == gridDim.x - 1) {
+        p.hdr[1] = 0u;
+        p.hdr[0] = epoch;
+      }
+    }
     const uint32_t stg_base = smem_u32(stg) + ew * 2 * kStageBuf;
     uint32_t sbuf = 0;  // staging buffer toggle of this warp
     uint64_t split_tiles[1];
@@ -855,6 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (leader) {
       split_smem[0] = split_tiles[0];
       nsplit_smem[0] = n_split;
+      nsplit_smem[3] = epoch;
     }
     if (lane == 0) bulk_wait<0>();  // staging must outlive the in-flight TMA stores
   }
@@ -874,7 +890,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (s.sk_tiles) {
     const uint32_t ft = threadIdx.x;
     const uint32_t n_split = nsplit_smem[0];
-    const uint32_t epoch = ld_relaxed_gpu(p.hdr) + 1u;
+    const uint32_t epoch = nsplit_smem[3];  // read by the epilogue leader at kernel start
     constexpr uint32_t V = BN / 4;  // float4 column groups per tile row
     static_assert(C::RING_BYTES >= (uint32_t)kBM * (V + 1) * 16, "phase-2 band stage");
     const float4* wsv = reinterpret_cast<const float4*>(p.ws);
@@ -938,17 +954,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       phase2_bar_sync();  // stage and nsplit_smem[1..2] are reused by the next split tile
     }
     if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
-    // ---- launch epilogue: the last CTA out advances the workspace epoch
-    phase2_bar_sync();
-    if (ft == 0) {
-      __threadfence();
-      const uint32_t done = atomicAdd(p.hdr + 1, 1u);
-      if (done == gridDim.x - 1) {
-        p.hdr[1] = 0u;
-        __threadfence();
-        p.hdr[0] = epoch;
-      }
-    }
   }
 
   tc_fence_before();

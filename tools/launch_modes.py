@@ -18,7 +18,7 @@ def main():
     m, n, k = (int(v) for v in (sys.argv[1:4] if len(sys.argv) > 3 else (512, 512, 16384)))
     pol = sys.argv[4] if len(sys.argv) > 4 else "ask"
     tile = sk.TileShape(*(int(v) for v in (sys.argv[5] if len(sys.argv) > 5 else "128x128x64").split("x")))
-    sets = max(2, (512 << 20) // (2 * (m * k + k * n) + 4 * m * n))
+    sets = min(64, max(2, (512 << 20) // (2 * (m * k + k * n) + 4 * m * n)))
     ops = [(torch.randn(m, k, device="cuda").to(torch.bfloat16), torch.randn(k, n, device="cuda").to(torch.bfloat16),
             torch.empty(m, n, device="cuda")) for _ in range(sets)]
     steps = 2000 // sets * sets

@@ -78,8 +78,11 @@ def main() -> None:
                   f"(+{gap:5.0f}) lat {lat:6.0f}")
         if n > 8:
             print(f"  mean arrival spacing k>=8: {(ks[n - 1, 1] - ks[8, 1]) / (n - 9):.0f} cycles")
-    for x in range(min(args.per_cta, plan.g)):
-        row = [(t[x, i] - base) / 1e3 if t[x, i] > 0 else float('nan') for i in range(7)]
+    cols = [0, 3, 8, 10, 4, 5, 11, 12, 6]  # start mma_done epi_first part_flag phase1 waited sum1 sum2 phase2
+    if args.per_cta:
+        print("  cta      " + " ".join(f"{EVENTS[i][:7]:>7s}" for i in cols))
+    for x in range(min(args.per_cta, grid)):
+        row = [(t[x, i] - base) / 1e3 if t[x, i] > 0 else float('nan') for i in cols]
         print(f"  cta {x:3d}: " + " ".join(f"{v:7.2f}" for v in row))
 
 
