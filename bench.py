@@ -473,7 +473,7 @@ def run_ours(args, wl: dict) -> None:
             "e2e": {
                 "value": round(e2e_value, 3), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": int(2 * (m * k + k * n)), "d2h_bytes_per_step": int(4 * m * n),
-                "api": "paper_2408_11417_b200.execute_schedule(pinned host bf16 tensors)",
+                "api": f"paper_2408_11417_b200.execute_schedule(pinned host {wl['dtype']} tensors)",
                 "steps": e2e_steps,
             },
             "isolated_launch": {
