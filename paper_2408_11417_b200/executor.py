@@ -379,7 +379,13 @@ def execute_schedule(
     GemmPlan(ad, bd, c, sched.policy, tile, sched.g).launch()
     out = c[:, : size.n]
     if is_torch:
-        return out.cpu() if host_result else out
+        if not host_result:
+            return out
+        # pinned staging (torch's caching host allocator): ~4x faster D2H than pageable
+        host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        host.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(ad.device).synchronize()
+        return host
     return out.to(torch.float64).cpu().numpy()
 
 
