@@ -142,6 +142,10 @@ void skpp_set_pdl(int enable);
 /* Load each stage's B columns with one 3-D TMA box when N % 64 == 0 (default on;
    plans created after the call). */
 void skpp_set_b3d(int enable);
+/* L2 cache-policy hints on the operand stream (default on; plans created after the call):
+   B k-blocks are loaded evict_last (the next wave of tiles re-reads them), C tiles are
+   stored evict_first. */
+void skpp_set_l2_hints(int enable);
 /* SM count, compute capability and the co-resident CTA limit of the GEMM kernel for blk_n. */
 int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 int skpp_max_coresident(const skpp_tile_t* t, int32_t* ctas);

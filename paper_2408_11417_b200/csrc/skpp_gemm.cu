@@ -134,6 +134,60 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
       "r"(c0), "r"(c1), "r"(smem_u32(src))
       : "memory");
 }
+// L2 cache-policy variants (createpolicy): B k-slices are re-read by the next wave
+// (evict_last); C tiles are written once (evict_first).
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                 int32_t c2, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* map, int32_t c0,
+                                                      int32_t c1, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_hint(void* dst, const CUtensorMap* map, int32_t c0,
+                                                      int32_t c1, int32_t c2, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar) & 0xFEFFFFFFu),
+      "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int32_t c0,
+                                                  int32_t c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -341,6 +395,7 @@ struct GemmParams {
   int64_t* trace_counts;
   uint64_t* timeline;  // debug: TL_EVENTS %globaltimer stamps per CTA, or null
   uint32_t b3d;         // tmB is the 3-D (n64, k, chunk) map: one B load per stage
+  uint32_t l2_hints;    // B loads evict_last, C stores evict_first (skpp_set_l2_hints)
 };
 
 // Debug timeline (skpp_debug_timeline): per-CTA %globaltimer stamps.
@@ -636,15 +691,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     // throughput limit of its own; each arrives once per stage on the full
     // barrier with its own byte count.
     const bool load_a = warp == 0;
-    uint32_t stage = 0, phase = 0, kcount = 0;
+    uint32_t stage = 0, phase = 0, kcount = 0, n_full = 0;
     bool first_load = true;
+    const uint64_t pol_b = l2_policy_evict_last();
     Cursor cur;
     cursor_init(cur, s, x);
     Item it;
     while (cursor_next(cur, s, x, it)) {
       const int32_t m0 = (int32_t)((it.tile / s.n_tiles) * TILE_M + rank * kBM);
       const int32_t n0 = (int32_t)((it.tile % s.n_tiles) * BN + rank * C::BNC);
-      for (uint64_t kk = it.kb; kk < it.ke; ++kk) {
+      // Serpentine K: every other FULL item of this workgroup walks K backwards.  A
+      // workgroup's consecutive FULL items run in consecutive waves, and every
+      // workgroup of a wave streams (nearly) all of B; walking the next wave's K in
+      // the opposite direction starts it on the k-slices the previous wave touched
+      // last, which are still in L2.  Only the order of the fp32 accumulation inside
+      // a tile changes (fixed per tile => deterministic); the MMA warp only counts stages.
+      const bool reverse = it.role == ROLE_FULL && (n_full++ & 1u);
+      for (uint64_t i = 0; i < it.ke - it.kb; ++i) {
+        const uint64_t kk = reverse ? it.ke - 1 - i : it.kb + i;
         mbar_wait(&empty_bar[stage], phase ^ 1, 1);
         if (load_a) {
           SKPP_KSTAMP(p, kcount, 0);
@@ -664,7 +728,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (uint32_t j = 0; j < C::A_OPS; ++j)
               tma_load_2d(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
           } else if (p.b3d) {  // all of the stage's B columns in one 3-D box
-            tma_load_3d(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
+            if (p.l2_hints)
+              tma_load_3d_hint(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage], pol_b);
+            else
+              tma_load_3d(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
           } else {
 #pragma unroll
             for (int j = 0; j < C::BNC / 64; ++j)
@@ -677,7 +744,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (uint32_t j = 0; j < C::A_OPS; ++j)
               tma_load_2d_pair(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
           } else if (p.b3d) {
-            tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
+            if (p.l2_hints)
+              tma_load_3d_pair_hint(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage], pol_b);
+            else
+              tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage]);
           } else {
 #pragma unroll
             for (int j = 0; j < C::BNC / 64; ++j)
@@ -765,6 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const uint32_t stg_base = smem_u32(stg) + ew * 2 * kStageBuf;
     uint32_t sbuf = 0;  // staging buffer toggle of this warp
+    const uint64_t pol_c = l2_policy_evict_first();
     uint64_t split_tiles[1];
     uint32_t n_split = 0, sk_seen = 0, local = 0;
     Cursor cur;
@@ -850,8 +921,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_async_shared();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmC, stg + (buf - smem_u32(stg)), (int32_t)(tile_col0 + c * ccols),
-                           (int32_t)(tile_row0 + ew * 32));
+              if (p.l2_hints)
+                tma_store_2d_hint(&tmC, stg + (buf - smem_u32(stg)), (int32_t)(tile_col0 + c * ccols),
+                                  (int32_t)(tile_row0 + ew * 32), pol_c);
+              else
+                tma_store_2d(&tmC, stg + (buf - smem_u32(stg)), (int32_t)(tile_col0 + c * ccols),
+                             (int32_t)(tile_row0 + ew * 32));
               bulk_commit();
             }
             sbuf ^= 1;
@@ -1057,6 +1132,7 @@ static void sched_from_c(const skpp_sched_t& c, Sched& s) {
 static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
 static int g_pdl = 1;                    // skpp_set_pdl
 static int g_b3d = 1;                    // skpp_set_b3d
+static int g_l2_hints = 1;               // skpp_set_l2_hints
 
 // A prepared launch: tensor maps, parameters and kernel, built once.
 struct Plan {
@@ -1224,6 +1300,7 @@ extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_til
 extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
 extern "C" void skpp_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 extern "C" void skpp_set_b3d(int enable) { g_b3d = enable ? 1 : 0; }
+extern "C" void skpp_set_l2_hints(int enable) { g_l2_hints = enable ? 1 : 0; }
 
 extern "C" int skpp_set_device(int device) {
   cudaError_t e = cudaSetDevice(device);
@@ -1384,6 +1461,7 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
              ((uint32_t)(t->blk_n >> 3) << 17) | ((uint32_t)(t->blk_m >> 4) << 24);
   gp.out_dtype = ops->out_dtype;
   gp.b3d = b3d ? 1 : 0;
+  gp.l2_hints = g_l2_hints ? 1 : 0;
   gp.C = ops->c;
   gp.ldc = (uint64_t)ops->ldc;
   const uint32_t esz = ops->out_dtype == SKPP_F32 ? 4 : 2;

@@ -13,6 +13,9 @@ def main():
 
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import _lib
+
+    if os.environ.get("SKPP_L2_HINTS"):
+        _lib.lib.skpp_set_l2_hints(int(os.environ["SKPP_L2_HINTS"]))
     from tools.profile_gemm import parse_policy
 
     m, n, k = (int(v) for v in (sys.argv[1:4] if len(sys.argv) > 3 else (512, 512, 16384)))

@@ -46,6 +46,9 @@ def main() -> None:
 
     from paper_2408_11417_b200 import _lib
 
+    if os.environ.get("SKPP_L2_HINTS"):
+        _lib.lib.skpp_set_l2_hints(int(os.environ["SKPP_L2_HINTS"]))
+
     _lib.lib.skpp_set_b3d(args.b3d)
     dt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
     od = {"fp32": torch.float32, "bf16": torch.bfloat16, "fp16": torch.float16}[args.out]
