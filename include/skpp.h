@@ -146,6 +146,10 @@ void skpp_set_b3d(int enable);
    B k-blocks are loaded evict_last (the next wave of tiles re-reads them), C tiles are
    stored evict_first. */
 void skpp_set_l2_hints(int enable);
+/* Test hooks (plans created after the call): bit 0 forces the two-pass Stream-K fixup
+   (peers first, owner added in a second pass) even when the owner is already published;
+   results are bit-identical to the one-pass path by construction (tests check it). */
+void skpp_set_debug(int flags);
 /* SM count, compute capability and the co-resident CTA limit of the GEMM kernel for blk_n. */
 int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 int skpp_max_coresident(const skpp_tile_t* t, int32_t* ctas);

@@ -129,6 +129,7 @@ SIGNATURES = {
     "skpp_set_pdl": (None, [C.c_int]),
     "skpp_set_b3d": (None, [C.c_int]),
     "skpp_set_l2_hints": (None, [C.c_int]),
+    "skpp_set_debug": (None, [C.c_int]),
     "skpp_device_info": (C.c_int, [C.c_int, _P(C.c_int32), _P(C.c_int32), _P(C.c_int32)]),
     "skpp_max_coresident": (C.c_int, [_P(Tile), _P(C.c_int32)]),
     "skpp_murmur3_x64_128": (None, [C.c_char_p, C.c_uint64, C.c_uint32, _u64p]),

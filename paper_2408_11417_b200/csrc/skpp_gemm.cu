@@ -396,6 +396,7 @@ struct GemmParams {
   uint64_t* timeline;  // debug: TL_EVENTS %globaltimer stamps per CTA, or null
   uint32_t b3d;         // tmB is the 3-D (n64, k, chunk) map: one B load per stage
   uint32_t l2_hints;    // B loads evict_last, C stores evict_first (skpp_set_l2_hints)
+  uint32_t debug;       // skpp_set_debug: bit 0 = always take the two-pass (owner-late) fixup path
 };
 
 // Debug timeline (skpp_debug_timeline): per-CTA %globaltimer stamps.
@@ -1014,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       phase2_bar_sync();
       if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
-      const bool owner_ready = nsplit_smem[1] != 0;
+      const bool owner_ready = nsplit_smem[1] != 0 && !(p.debug & 1u);
       const uint32_t nrows = R1 - R0;
       band_reduce<CG>(ra, R0, nrows, V, 0, owner_ready ? nc : nc - 1, false, stage, ft);
       if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM1);
@@ -1133,6 +1134,7 @@ static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
 static int g_pdl = 1;                    // skpp_set_pdl
 static int g_b3d = 1;                    // skpp_set_b3d
 static int g_l2_hints = 1;               // skpp_set_l2_hints
+static int g_debug = 0;                  // skpp_set_debug
 
 // A prepared launch: tensor maps, parameters and kernel, built once.
 struct Plan {
@@ -1301,6 +1303,7 @@ extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = devi
 extern "C" void skpp_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 extern "C" void skpp_set_b3d(int enable) { g_b3d = enable ? 1 : 0; }
 extern "C" void skpp_set_l2_hints(int enable) { g_l2_hints = enable ? 1 : 0; }
+extern "C" void skpp_set_debug(int flags) { g_debug = flags; }
 
 extern "C" int skpp_set_device(int device) {
   cudaError_t e = cudaSetDevice(device);
@@ -1462,6 +1465,7 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   gp.out_dtype = ops->out_dtype;
   gp.b3d = b3d ? 1 : 0;
   gp.l2_hints = g_l2_hints ? 1 : 0;
+  gp.debug = (uint32_t)g_debug;
   gp.C = ops->c;
   gp.ldc = (uint64_t)ops->ldc;
   const uint32_t esz = ops->out_dtype == SKPP_F32 ? 4 : 2;

@@ -170,3 +170,44 @@ def test_randn_within_tolerance_and_deterministic():
         again = sk.gemm(a, b, sk.Policy.all_stream_k())
         torch.cuda.synchronize()
         assert torch.equal(again, base)
+
+
+@pytest.mark.parametrize("tile", [(128, 128, 64), (128, 128, 128), (256, 256, 128)])
+def test_fixup_one_pass_and_two_pass_paths_bit_identical(tile):
+    """The phase-2 fixup sums (((0 + p1) + p2) ... ) + p0 whether the owner's partial is
+    added in the same pass (owner already published) or in a second pass (owner late);
+    skpp_set_debug(1) forces the second path.  randn inputs, so rounding would show."""
+    sk = _sk()
+    from paper_2408_11417_b200 import _lib
+
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    m, n, k = 512, 768, 8192
+    a = torch.randn(m, k, generator=gen, device="cuda").to(torch.bfloat16)
+    b = torch.randn(k, n, generator=gen, device="cuda").to(torch.bfloat16)
+    t = sk.TileShape(*tile)
+    outs = []
+    try:
+        for flags in (0, 1):
+            _lib.lib.skpp_set_debug(flags)
+            for pol in (sk.Policy.all_stream_k(), sk.Policy.hybrid(2, sk_first=False)):
+                c = torch.empty(m, n, device="cuda")
+                sk.GemmPlan(a, b, c, pol, t).launch()
+                torch.cuda.synchronize()
+                outs.append(c)
+    finally:
+        _lib.lib.skpp_set_debug(0)
+    assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[3])
+
+
+@pytest.mark.parametrize("tile", [(128, 128, 64), (128, 128, 128), (256, 256, 128)])
+def test_multi_wave_serpentine_k_bitwise(tile):
+    """Several data-parallel waves per workgroup (odd waves walk K backwards), ragged K
+    tail inside the first reversed k-block; integer inputs => exact in any order."""
+    sk = _sk()
+    m, n, k = 2048, 2560, 1096
+    a, b = _int_case(m, n, k, seed=11)
+    want = ogemm.reference_gemm(a, b)
+    for pol in (sk.Policy.data_parallel(), sk.Policy.hybrid(1), sk.Policy.hybrid(2, sk_first=False)):
+        got, _ = _run(a, b, pol, sk.TileShape(*tile))
+        assert np.array_equal(got.double().cpu().numpy(), want), pol.label
