@@ -28,6 +28,9 @@ def main() -> None:
 
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import _lib
+
+    if os.environ.get("SKPP_DEBUG"):
+        _lib.lib.skpp_set_debug(int(os.environ["SKPP_DEBUG"]))
     from tools.profile_gemm import parse_policy
 
     tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
