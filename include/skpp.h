@@ -142,6 +142,12 @@ void skpp_set_pdl(int enable);
 /* Load each stage's B columns with one 3-D TMA box when N % 64 == 0 (default on;
    plans created after the call). */
 void skpp_set_b3d(int enable);
+/* Load a BK=128 stage's A rows with one 3-D TMA box when K % 64 == 0 (default on; plans
+   created after the call). */
+void skpp_set_a3d(int enable);
+/* k-blocks of each workgroup's first item to prefetch into L2 before the kernel waits on
+   the previous grid (PDL); 0 disables (plans created after the call). */
+void skpp_set_l2_prefetch(int k_blocks);
 /* L2 cache-policy hints on the operand stream (default on; plans created after the call):
    B k-blocks are loaded evict_last (the next wave of tiles re-reads them), C tiles are
    stored evict_first. */

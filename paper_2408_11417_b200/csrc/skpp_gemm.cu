@@ -188,6 +188,22 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const 
       : "memory");
 }
 
+// L2 prefetch of a tensor box (no shared memory, no barrier).  Safe before
+// griddepcontrol.wait: L2 is the point of coherence, so a line the previous kernel
+// still writes is updated in place; the prefetch can only be wasted, never stale.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -395,6 +411,8 @@ struct GemmParams {
   int64_t* trace_counts;
   uint64_t* timeline;  // debug: TL_EVENTS %globaltimer stamps per CTA, or null
   uint32_t b3d;         // tmB is the 3-D (n64, k, chunk) map: one B load per stage
+  uint32_t a3d;         // tmA is the 3-D (k64, row, chunk) map: one A load per BK=128 stage
+  uint32_t l2_prefetch; // k-blocks of the first item prefetched to L2 before griddepcontrol.wait
   uint32_t l2_hints;    // B loads evict_last, C stores evict_first (skpp_set_l2_hints)
   uint32_t debug;       // skpp_set_debug: bit 0 = always take the two-pass (owner-late) fixup path
 };
@@ -678,9 +696,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // While the previous kernel drains, pull the first `p.l2_prefetch` k-blocks of this
+  // workgroup's first item into L2 (A by warp 0, B by warp 3), so the first stages
+  // land from L2 right after the wait below.
+  if ((warp == 0 || warp == 3) && lane == 0 && p.l2_prefetch) {
+    Cursor c0;
+    cursor_init(c0, s, x);
+    Item it0;
+    if (cursor_next(c0, s, x, it0)) {
+      const int32_t m0 = (int32_t)((it0.tile / s.n_tiles) * TILE_M + rank * kBM);
+      const int32_t n0 = (int32_t)((it0.tile % s.n_tiles) * BN + rank * C::BNC);
+      const uint64_t kend = it0.kb + p.l2_prefetch < it0.ke ? it0.kb + p.l2_prefetch : it0.ke;
+      for (uint64_t kk = it0.kb; kk < kend; ++kk) {
+        const int32_t k0 = (int32_t)(kk * BK);
+        if (warp == 0) {
+          if (C::A_OPS > 1 && p.a3d)
+            tma_prefetch_3d(&tmA, 0, m0, k0 / 64);
+          else
+            for (uint32_t j = 0; j < C::A_OPS; ++j) tma_prefetch_2d(&tmA, k0 + 64 * j, m0);
+        } else if (p.b3d) {
+          tma_prefetch_3d(&tmB, 0, k0, n0 / 64);
+        } else {
+          for (int j = 0; j < C::BNC / 64; ++j) tma_prefetch_2d(&tmB, n0 + 64 * j, k0);
+        }
+      }
+    }
+  }
   // Programmatic dependent launch: everything above (barrier init, TMEM
-  // allocation, descriptor prefetch) overlaps the previous kernel's tail; no
-  // global memory written by earlier work is touched before this wait.
+  // allocation, descriptor and L2 prefetch) overlaps the previous kernel's tail;
+  // no global memory written by earlier work is read before this wait.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) SKPP_STAMP(p, TL_START);
@@ -725,9 +769,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t k0 = (int32_t)(kk * BK);
         if constexpr (CG == 1) {
           if (load_a) {
+            if (C::A_OPS > 1 && p.a3d) {  // both 64-deep sub-tiles in one 3-D box
+              tma_load_3d(sA + stage * C::A_BYTES, &tmA, 0, m0, k0 / 64, &full_bar[stage]);
+            } else {
 #pragma unroll
-            for (uint32_t j = 0; j < C::A_OPS; ++j)
-              tma_load_2d(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
+              for (uint32_t j = 0; j < C::A_OPS; ++j)
+                tma_load_2d(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
+            }
           } else if (p.b3d) {  // all of the stage's B columns in one 3-D box
             if (p.l2_hints)
               tma_load_3d_hint(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage], pol_b);
@@ -741,9 +789,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           if (load_a) {
+            if (C::A_OPS > 1 && p.a3d) {
+              tma_load_3d_pair(sA + stage * C::A_BYTES, &tmA, 0, m0, k0 / 64, &full_bar[stage]);
+            } else {
 #pragma unroll
-            for (uint32_t j = 0; j < C::A_OPS; ++j)
-              tma_load_2d_pair(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
+              for (uint32_t j = 0; j < C::A_OPS; ++j)
+                tma_load_2d_pair(sA + stage * C::A_BYTES + j * C::A_SUB, &tmA, k0 + 64 * j, m0, &full_bar[stage]);
+            }
           } else if (p.b3d) {
             if (p.l2_hints)
               tma_load_3d_pair_hint(sB + stage * C::B_BYTES, &tmB, 0, k0, n0 / 64, &full_bar[stage], pol_b);
@@ -1133,6 +1185,8 @@ static void sched_from_c(const skpp_sched_t& c, Sched& s) {
 static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
 static int g_pdl = 1;                    // skpp_set_pdl
 static int g_b3d = 1;                    // skpp_set_b3d
+static int g_a3d = 1;                    // skpp_set_a3d
+static int g_l2_prefetch = 2;            // skpp_set_l2_prefetch (k-blocks)
 static int g_l2_hints = 1;               // skpp_set_l2_hints
 static int g_debug = 0;                  // skpp_set_debug
 
@@ -1302,6 +1356,8 @@ extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_til
 extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
 extern "C" void skpp_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 extern "C" void skpp_set_b3d(int enable) { g_b3d = enable ? 1 : 0; }
+extern "C" void skpp_set_a3d(int enable) { g_a3d = enable ? 1 : 0; }
+extern "C" void skpp_set_l2_prefetch(int k_blocks) { g_l2_prefetch = k_blocks > 0 ? k_blocks : 0; }
 extern "C" void skpp_set_l2_hints(int enable) { g_l2_hints = enable ? 1 : 0; }
 extern "C" void skpp_set_debug(int flags) { g_debug = flags; }
 
@@ -1428,7 +1484,27 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
                                   : BK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                              : CU_TENSOR_MAP_SWIZZLE_32B;
   const CUtensorMapDataType in_dt = map_dtype(ops->in_dtype);
-  rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK > 64 ? 64 : BK, kBM, aswz);
+  // BK = 128 with K % 64 == 0: A as (k in chunk, row, 64-deep chunk) so one 3-D box fills
+  // both sub-tiles [chunk][128 rows][64] (the per-SM TMA stage rate falls with fewer ops).
+  // Otherwise a chunk could run past a row end, so two 2-D boxes per stage.
+  const bool a3d = g_a3d && BK > 64 && p->k % 64 == 0;
+  if (a3d) {
+    auto fn = encode_fn();
+    const cuuint64_t dims[3] = {64, p->m, p->k / 64};
+    const cuuint64_t strides[2] = {(cuuint64_t)ops->lda * 2, 128};
+    const cuuint32_t box[3] = {64, (cuuint32_t)kBM, BK / 64};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn ? fn(&pl->ma, in_dt, 3, const_cast<void*>(ops->a), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+                    : CUDA_ERROR_NOT_SUPPORTED;
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (3-D A) failed with CUresult " + std::to_string((int)r));
+      rc = SKPP_ELAUNCH;
+    }
+  } else {
+    rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK > 64 ? 64 : BK, kBM, aswz);
+  }
   const uint32_t bnc = t->blk_n / (t->blk_m / kBM);  // B columns per CTA
   const bool b3d = g_b3d && p->n % 64 == 0 && bnc > 64;
   if (!rc && b3d) {
@@ -1464,6 +1540,8 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
              ((uint32_t)(t->blk_n >> 3) << 17) | ((uint32_t)(t->blk_m >> 4) << 24);
   gp.out_dtype = ops->out_dtype;
   gp.b3d = b3d ? 1 : 0;
+  gp.a3d = a3d ? 1 : 0;
+  gp.l2_prefetch = (uint32_t)g_l2_prefetch;
   gp.l2_hints = g_l2_hints ? 1 : 0;
   gp.debug = (uint32_t)g_debug;
   gp.C = ops->c;

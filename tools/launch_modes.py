@@ -14,6 +14,10 @@ def main():
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import _lib
 
+    if os.environ.get("SKPP_PF"):
+        _lib.lib.skpp_set_l2_prefetch(int(os.environ["SKPP_PF"]))
+    if os.environ.get("SKPP_A3D"):
+        _lib.lib.skpp_set_a3d(int(os.environ["SKPP_A3D"]))
     if os.environ.get("SKPP_L2_HINTS"):
         _lib.lib.skpp_set_l2_hints(int(os.environ["SKPP_L2_HINTS"]))
     from tools.profile_gemm import parse_policy
