@@ -202,8 +202,11 @@ def tune_sizes(
     params: MeasureParams | None = None,
     pool: OperandPool | None = None,
     progress=None,
+    seconds: dict | None = None,
 ) -> list[TuneRecord]:
-    """Measured records for ``sizes`` on the current device, in input order."""
+    """Measured records for ``sizes`` on the current device, in input order.  With
+    ``seconds``, each size's measurement wall time is added to ``seconds[size]``
+    (the cost table a later sweep can partition by)."""
     if policies is None:
         policies = canonical_policies()
     if params is None:
@@ -214,7 +217,10 @@ def tune_sizes(
         pool = OperandPool(sizes, params.in_dtype, params.out_dtype)
     out = []
     for i, size in enumerate(sizes):
+        t0 = time.perf_counter() if seconds is not None else 0.0
         out.append(measure_size(size, tile, g, policies, params, pool))
+        if seconds is not None:
+            seconds[size] = seconds.get(size, 0.0) + time.perf_counter() - t0
         if progress is not None:
             progress(i + 1, len(sizes))
     return out
@@ -237,6 +243,40 @@ def estimated_cost_s(size: ProblemSize, n_policies: int = 7, peak_tflops: float 
     tiles = -(-size.m // tile_mn) * -(-size.n // tile_mn)
     distinct = 2 if tiles <= sms else n_policies
     return distinct * (fixed_s + (4 + inner * (1 + reps)) * t_us * 1e-6)
+
+
+def save_cost_table(path: str, seconds: dict) -> None:
+    """Per-size measurement wall times of a sweep ({"m,n,k": s}), for :func:`measured_cost`."""
+    import json
+
+    with open(path, "w") as fh:
+        json.dump({f"{z.m},{z.n},{z.k}": round(v, 6) for z, v in sorted(
+            seconds.items(), key=lambda kv: (kv[0].m, kv[0].n, kv[0].k))}, fh)
+
+
+def load_cost_table(paths) -> dict:
+    import json
+
+    table = {}
+    for path in paths:
+        with open(path) as fh:
+            for key, v in json.load(fh).items():
+                m, n, k = (int(x) for x in key.split(","))
+                table[ProblemSize(m, n, k)] = float(v)
+    return table
+
+
+def measured_cost(table: dict, fallback=estimated_cost_s):
+    """LPT cost = a previous sweep's measured wall time for the size (the best predictor of
+    the next one), scaled to the analytic model's units for sizes it did not see."""
+    known = [z for z in table if table[z] > 0]
+    scale = (sum(table[z] for z in known) / sum(fallback(z) for z in known)) if known else 1.0
+
+    def cost(size: ProblemSize) -> float:
+        v = table.get(size)
+        return v if v is not None and v > 0 else scale * fallback(size)
+
+    return cost
 
 
 def lpt_partition(sizes: list[ProblemSize], world: int, cost=estimated_cost_s) -> list[list[ProblemSize]]:
@@ -322,22 +362,25 @@ def gpu_measure(tile: TileShape, policies: list[Policy] | None = None, params: M
 
 
 def run_shard_tiles(sizes: list[ProblemSize], rank: int, world: int, tiles: list[TileShape],
-                    params: MeasureParams, out_dir: str, tag: str = "records") -> None:
-    """Measure this rank's LPT share of ``sizes`` under every tile; one CSV shard per tile."""
+                    params: MeasureParams, out_dir: str, tag: str = "records", cost=estimated_cost_s) -> None:
+    """Measure this rank's LPT share of ``sizes`` under every tile; one CSV shard per tile,
+    plus ``costs.<tag>.rank<r>.json`` (per-size measurement seconds, summed over tiles)."""
     import os
 
     from .pipeline import write_records_csv
     from .tiles import tile_label
 
-    mine = lpt_partition(sizes, world)[rank]
+    mine = lpt_partition(sizes, world, cost)[rank]
     mine.sort(key=lambda s: (s.m, s.n, s.k))
     pool = OperandPool(mine, params.in_dtype, params.out_dtype) if mine else None
+    seconds: dict = {}
     for tile in tiles:
         path = os.path.join(out_dir, f"{tag}.{tile_label(tile)}.rank{rank}.csv")
         if mine:
-            write_records_csv(path, tune_sizes(mine, tile, None, None, params, pool))
+            write_records_csv(path, tune_sizes(mine, tile, None, None, params, pool, seconds=seconds))
         else:
             open(path, "w").close()
+    save_cost_table(os.path.join(out_dir, f"costs.{tag}.rank{rank}.json"), seconds)
 
 
 def merge_tiles(out_dir: str, world: int, tiles: list[TileShape], tag: str = "records"):
@@ -398,6 +441,9 @@ def main(argv=None) -> int:
     ap.add_argument("--max-gflop", type=float, default=0.0, help="skip sizes above this (0 = no limit)")
     ap.add_argument("--validate", action="store_true", help="re-measure everything (held-out run)")
     ap.add_argument("--heldout", type=int, default=0, help="also measure N off-grid sizes")
+    ap.add_argument("--cost-table", default="",
+                    help="comma list of costs.*.json from an earlier sweep: LPT partitions by the measured "
+                         "per-size times instead of the analytic estimate")
     ap.add_argument("--emulate-world", default="",
                     help="comma list of world sizes: run every rank's LPT share back to back on this GPU "
                          "and report max-over-ranks time per world size (single-GPU scaling estimate)")
@@ -425,9 +471,10 @@ def main(argv=None) -> int:
         if dist is not None:
             dist.barrier()
 
+    cost = measured_cost(load_cost_table(args.cost_table.split(","))) if args.cost_table else estimated_cost_s
     sw = Stopwatch()
     with sw:
-        run_shard_tiles(sizes, rank, world, tiles, params, args.out, "records")
+        run_shard_tiles(sizes, rank, world, tiles, params, args.out, "records", cost)
     with open(os.path.join(args.out, f"timing.rank{rank}.json"), "w") as fh:
         json.dump({"rank": rank, "world": world, "seconds": sw.seconds, "tiles": len(tiles)}, fh)
     if args.validate:
@@ -497,26 +544,43 @@ def emulate_worlds(args) -> int:
     tune_sizes(sizes[:3], tiles[0], None, None, params, pool)
     out = {"mode": "emulated: each rank's share measured back to back on one GPU; "
                    "wall time of a world = max over its ranks", "sizes": len(sizes),
-           "tiles": [tile_label(t) for t in tiles], "policies": 7, "worlds": {}}
-    for world in (int(w) for w in args.emulate_world.split(",")):
-        parts = lpt_partition(sizes, world)
-        secs = []
-        for part in parts:
-            part = sorted(part, key=lambda s: (s.m, s.n, s.k))
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for tile in tiles:
-                tune_sizes(part, tile, None, None, params, pool)
-            torch.cuda.synchronize()
-            secs.append(time.perf_counter() - t0)
-        pairs = len(sizes) * 7 * len(tiles)
-        out["worlds"][str(world)] = {
-            "rank_seconds": [round(v, 3) for v in secs],
-            "max_rank_seconds": round(max(secs), 3),
-            "shape_policy_per_s": round(pairs / max(secs), 1),
-            "load_imbalance": round(max(secs) / (sum(secs) / len(secs)), 3),
-        }
-        print(json.dumps({world: out["worlds"][str(world)]}), flush=True)
+           "tiles": [tile_label(t) for t in tiles], "policies": 7}
+    # World 1 measures every size once and records its wall time; larger worlds are then
+    # partitioned both by the analytic estimate and by those measured times (what a re-tune
+    # with a previous sweep's cost table does, --cost-table).
+    table: dict = {}
+    worlds = [int(w) for w in args.emulate_world.split(",")]
+    if 1 not in worlds:
+        worlds = [1] + worlds
+    for label, key in (("analytic", "worlds_analytic_cost"), ("measured", "worlds")):
+        out[key] = {}
+        for world in worlds:
+            if label == "measured" and world == 1:
+                out[key]["1"] = out["worlds_analytic_cost"]["1"]
+                continue
+            cost = estimated_cost_s if label == "analytic" else measured_cost(table)
+            parts = lpt_partition(sizes, world, cost)
+            secs = []
+            for part in parts:
+                part = sorted(part, key=lambda s: (s.m, s.n, s.k))
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for tile in tiles:
+                    tune_sizes(part, tile, None, None, params, pool,
+                               seconds=table if (label == "analytic" and world == 1) else None)
+                torch.cuda.synchronize()
+                secs.append(time.perf_counter() - t0)
+            pairs = len(sizes) * 7 * len(tiles)
+            out[key][str(world)] = {
+                "rank_seconds": [round(v, 3) for v in secs],
+                "max_rank_seconds": round(max(secs), 3),
+                "shape_policy_per_s": round(pairs / max(secs), 1),
+                "load_imbalance": round(max(secs) / (sum(secs) / len(secs)), 3),
+            }
+            print(json.dumps({label: {world: out[key][str(world)]}}), flush=True)
+    out["lpt_cost"] = {"worlds": "measured per-size times of the world-1 pass",
+                       "worlds_analytic_cost": "estimated_cost_s (analytic)"}
+    save_cost_table(os.path.join(args.out, "costs.emulate.json"), table)
     with open(os.path.join(args.out, "scaling_emulated.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     return 0

@@ -48,6 +48,29 @@ def test_lpt_partition_is_a_partition_and_balanced():
         assert max(loads) <= 1.05 * (sum(loads) / world) + max(sw.estimated_cost_s(s) for s in sizes)
 
 
+def test_measured_cost_table_round_trip_and_partition(tmp_path):
+    """A previous sweep's per-size wall times drive LPT; unseen sizes fall back to the
+    analytic estimate rescaled to the table's units."""
+    sizes = small_grid()
+    seen = sizes[: len(sizes) // 2]
+    times = {s: 1e-3 * (1 + (s.m * 7 + s.n * 3 + s.k) % 13) for s in seen}
+    path = tmp_path / "costs.json"
+    sw.save_cost_table(str(path), times)
+    table = sw.load_cost_table([str(path)])
+    assert set(table) == set(seen)
+    assert all(abs(table[s] - times[s]) < 1e-6 for s in seen)
+    cost = sw.measured_cost(table)
+    assert cost(seen[0]) == table[seen[0]]
+    unseen = sizes[-1]
+    scale = sum(table.values()) / sum(sw.estimated_cost_s(s) for s in seen)
+    assert abs(cost(unseen) - scale * sw.estimated_cost_s(unseen)) < 1e-12
+    for world in (2, 4, 8):
+        parts = sw.lpt_partition(sizes, world, cost)
+        assert sorted((s for p in parts for s in p), key=lambda s: (s.m, s.n, s.k)) == sizes
+        loads = [sum(cost(s) for s in p) for p in parts]
+        assert max(loads) <= sum(loads) / world + max(cost(s) for s in sizes)
+
+
 def test_shards_merge_to_the_single_process_bank(tmp_path):
     sizes = small_grid()
     single = fake_measure(sizes)
