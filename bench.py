@@ -56,7 +56,7 @@ WORKLOADS = {
                        desc="large square bf16 GEMM 8192^3, fp32 out (70%-of-peak target), Bloom-selected (tile, policy)"),
 }
 # Candidate tiles of the joint (tile, policy) selection, baseline (DP) tile first.
-BENCH_TILES = ["128x128x64", "128x128x128", "256x128x128", "256x256x64", "256x256x128"]
+BENCH_TILES = ["128x128x64", "128x64x128", "128x128x128", "256x128x128", "256x256x64", "256x256x128"]
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                   "source": "fallback (B200_PROFILING.md)"}
