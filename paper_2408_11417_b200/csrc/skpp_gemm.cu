@@ -415,6 +415,7 @@ struct GemmParams {
   uint32_t l2_prefetch; // k-blocks of the first item prefetched to L2 before griddepcontrol.wait
   uint32_t l2_hints;    // B loads evict_last, C stores evict_first (skpp_set_l2_hints)
   uint32_t debug;       // skpp_set_debug: bit 0 = always take the two-pass (owner-late) fixup path
+  uint32_t ragged;      // last row / column tile at most half full: partials and bands skip rows >= M, cols >= N
 };
 
 // Debug timeline (skpp_debug_timeline): per-CTA %globaltimer stamps.
@@ -544,9 +545,9 @@ __device__ __forceinline__ void st_shared_f4(uint32_t addr, float4 v) {
 template <int G, int KB>
 __device__ __noinline__ void band_sum(const float4* __restrict__ wsv, uint64_t slot_v, uint64_t peer_slot0,
                                       uint32_t peer_slot_step, uint64_t owner_slot, uint32_t nc,
-                                      uint32_t R0, uint32_t nrows, uint32_t V, uint32_t term_begin,
-                                      uint32_t term_end, uint32_t accumulate, uint32_t stage,
-                                      uint32_t ft) {
+                                      uint32_t R0, uint32_t nrows, uint32_t V, uint32_t sstride,
+                                      uint32_t term_begin, uint32_t term_end, uint32_t accumulate,
+                                      uint32_t stage, uint32_t ft) {
   const uint32_t total = nrows * V;
   for (uint32_t e0 = ft; e0 < total; e0 += G * kThreads) {
     float4 acc[G];
@@ -557,7 +558,7 @@ __device__ __noinline__ void band_sum(const float4* __restrict__ wsv, uint64_t s
       const uint32_t e = e0 + g * kThreads;
       const uint32_t j = e / nrows, ro = e - j * nrows;
       off[g] = j * kBM + R0 + ro;
-      saddr[g] = stage + (ro * (V + 1) + j) * 16;
+      saddr[g] = stage + (ro * sstride + j) * 16;
       acc[g] = (accumulate && e < total) ? ld_shared_f4(saddr[g]) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     for (uint32_t t0 = term_begin; t0 < term_end; t0 += KB) {
@@ -593,12 +594,13 @@ __device__ __noinline__ void band_sum(const float4* __restrict__ wsv, uint64_t s
 
 // Store the reduced band: consecutive threads take consecutive column groups of
 // one row, so a warp writes 512 contiguous bytes of C (fp32) per instruction.
+template <uint32_t V>
 __device__ __forceinline__ void band_store(const GemmParams& p, uint32_t stage, uint32_t nrows,
-                                           uint32_t V, uint64_t row0, uint64_t col0, uint32_t ft) {
+                                           uint32_t Vv, uint64_t row0, uint64_t col0, uint32_t ft) {
   const uint32_t total = nrows * V;
   for (uint32_t e = ft; e < total; e += kThreads) {
     const uint32_t ro = e / V, j = e - ro * V;
-    store_vec4(p, row0 + ro, col0 + 4 * j, ld_shared_f4(stage + (ro * (V + 1) + j) * 16));
+    if (j < Vv) store_vec4(p, row0 + ro, col0 + 4 * j, ld_shared_f4(stage + (ro * (V + 1) + j) * 16));
   }
 }
 
@@ -607,16 +609,18 @@ __device__ __forceinline__ void band_store(const GemmParams& p, uint32_t stage, 
 // loads, <= 24 float4 in flight per thread: larger variants spill, and a
 // cp.async variant (all terms' bands in flight through the idle ring) measured
 // 3-20% slower on every fixup-heavy shape tried (tools/ab_reduce.py).
-template <int CG>
+// V = column groups to reduce (<= BN/4 for a ragged last column tile); the stage
+// row stride is the tile's BN/4 + 1 (SV) for every tile.
+template <int CG, uint32_t SV>
 __device__ __forceinline__ void band_reduce(const ReduceArgs& ra, uint32_t R0, uint32_t nrows, uint32_t V,
                                             uint32_t term_begin, uint32_t term_end, bool accumulate,
                                             uint32_t stage, uint32_t ft) {
   const uint64_t peer0 = 2 * ((ra.x0 + 1) * CG + ra.rank);
   if (ra.nc <= 4)
-    band_sum<4, 4>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, term_begin, term_end,
+    band_sum<4, 4>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, SV + 1, term_begin, term_end,
                    accumulate, stage, ft);
   else
-    band_sum<2, 12>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, term_begin, term_end,
+    band_sum<2, 12>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, SV + 1, term_begin, term_end,
                     accumulate, stage, ft);
 }
 
@@ -910,20 +914,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         // store of one column group is 32 consecutive rows = 512 contiguous bytes,
         // and a contributor's share of columns is one contiguous range.
         float4* dst = reinterpret_cast<float4*>(p.ws + slot * (uint64_t)(kBM * BN)) + row;
+        // Only rows < M and columns < N are ever reduced (phase 2 bounds its bands the same
+        // way, at 32-row / 32-column granularity), so the partial of a ragged or skinny
+        // tile (decode-like M = 1..127) costs only its valid chunks on the SM's store port.
+        // Warp-uniform: a warp skips its 32 rows when they are all past M, and every warp
+        // skips the 32-column chunks past N.
+        const bool warp_rows_ok = tile_row0 + ew * 32 < p.M;
+        const uint64_t cols_left = p.N - tile_col0;
+        const int chunks_ok = cols_left >= (uint64_t)BN ? BN / 32 : (int)((cols_left + 31) / 32);
+        if (!p.ragged || (warp_rows_ok && chunks_ok == BN / 32)) {  // full tile: every row and column chunk
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t w[32];
-          tmem_ld_32(taddr + c * 32, w);
-          tmem_ld_wait();
-          if (c == BN / 32 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) release_acc(&tempty_bar[as]);
-          }
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t w[32];
+            tmem_ld_32(taddr + c * 32, w);
+            tmem_ld_wait();
+            if (c == BN / 32 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) release_acc(&tempty_bar[as]);
+            }
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[(c * 8 + j) * kBM] = make_float4(__uint_as_float(w[4 * j]), __uint_as_float(w[4 * j + 1]),
-                                                 __uint_as_float(w[4 * j + 2]), __uint_as_float(w[4 * j + 3]));
+            for (int j = 0; j < 8; ++j)
+              dst[(c * 8 + j) * kBM] = make_float4(__uint_as_float(w[4 * j]), __uint_as_float(w[4 * j + 1]),
+                                                   __uint_as_float(w[4 * j + 2]), __uint_as_float(w[4 * j + 3]));
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            if (warp_rows_ok && c < chunks_ok) {
+              uint32_t w[32];
+              tmem_ld_32(taddr + c * 32, w);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                dst[(c * 8 + j) * kBM] = make_float4(__uint_as_float(w[4 * j]), __uint_as_float(w[4 * j + 1]),
+                                                     __uint_as_float(w[4 * j + 2]), __uint_as_float(w[4 * j + 3]));
+            }
+            if (c == BN / 32 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) release_acc(&tempty_bar[as]);
+            }
+          }
         }
         if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_ISSUED);
         // publish: every thread's stores happen-before the barrier; the leader's
@@ -1033,8 +1065,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t r_lo = x0 + (aligned ? 0 : 1);
       const uint32_t nr = (uint32_t)(x1 - r_lo + 1);
       const uint32_t idx = (uint32_t)(x - r_lo);
-      const uint32_t R0 = (uint32_t)(((uint64_t)idx * kBM) / nr);
-      const uint32_t R1 = (uint32_t)(((uint64_t)(idx + 1) * kBM) / nr);
+      // ragged problems only (M or N not a multiple of the tile): bound the band by the
+      // rows / column chunks the contributors wrote (phase 1 skips the rest)
+      uint32_t rows_ok = kBM, Vv = V;
+      if (p.ragged) {
+        const uint64_t tile_rows0 = ((s.dp_tiles + u) / s.n_tiles) * TILE_M + rank * kBM;
+        if (tile_rows0 >= p.M)
+          rows_ok = 0;  // this row half of the tile is entirely past M: empty band below
+        else if (p.M - tile_rows0 < (uint64_t)kBM)
+          rows_ok = (uint32_t)((p.M - tile_rows0 + 31) / 32 * 32);
+        const uint64_t tile_cols0 = ((s.dp_tiles + u) % s.n_tiles) * BN;
+        if (p.N - tile_cols0 < (uint64_t)BN) Vv = (uint32_t)((p.N - tile_cols0 + 31) / 32 * 32 / 4);
+      }
+      const uint32_t R0 = (uint32_t)(((uint64_t)idx * rows_ok) / nr);
+      const uint32_t R1 = (uint32_t)(((uint64_t)(idx + 1) * rows_ok) / nr);
       if (R0 == R1) continue;
       // contributor x0+t wrote its first Stream-K item (slot 2*cta), except x0
       // when its range starts inside an earlier tile (tile u is its last item)
@@ -1069,16 +1113,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
       const bool owner_ready = nsplit_smem[1] != 0 && !(p.debug & 1u);
       const uint32_t nrows = R1 - R0;
-      band_reduce<CG>(ra, R0, nrows, V, 0, owner_ready ? nc : nc - 1, false, stage, ft);
+      band_reduce<CG, V>(ra, R0, nrows, Vv, 0, owner_ready ? nc : nc - 1, false, stage, ft);
       if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM1);
       if (!owner_ready) {
         if (ft == 0) wait_flag(p.flags + slot0, epoch);
         phase2_bar_sync();  // also orders the stage writes above before the re-reads below
-        band_reduce<CG>(ra, R0, nrows, V, nc - 1, nc, true, stage, ft);
+        band_reduce<CG, V>(ra, R0, nrows, Vv, nc - 1, nc, true, stage, ft);
         if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM2);
       }
       phase2_bar_sync();
-      band_store(p, stage, nrows, V, row0, gcol0, ft);
+      band_store<V>(p, stage, nrows, Vv, row0, gcol0, ft);
       phase2_bar_sync();  // stage and nsplit_smem[1..2] are reused by the next split tile
     }
     if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
@@ -1544,6 +1588,13 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   gp.l2_prefetch = (uint32_t)g_l2_prefetch;
   gp.l2_hints = g_l2_hints ? 1 : 0;
   gp.debug = (uint32_t)g_debug;
+  // Skip-invalid-rows/columns mode only where it saves at least half a tile of partial
+  // bytes (decode-like M, narrow N): on other shapes the bounds checks cost more than the
+  // 32-row / 32-column chunks they would skip.
+  {
+    const uint64_t mr = p->m % t->blk_m, nr = p->n % t->blk_n;
+    gp.ragged = ((mr != 0 && 2 * mr <= t->blk_m) || (nr != 0 && 2 * nr <= t->blk_n)) ? 1u : 0u;
+  }
   gp.C = ops->c;
   gp.ldc = (uint64_t)ops->ldc;
   const uint32_t esz = ops->out_dtype == SKPP_F32 ? 4 : 2;

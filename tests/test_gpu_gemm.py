@@ -211,3 +211,15 @@ def test_multi_wave_serpentine_k_bitwise(tile):
     for pol in (sk.Policy.data_parallel(), sk.Policy.hybrid(1), sk.Policy.hybrid(2, sk_first=False)):
         got, _ = _run(a, b, pol, sk.TileShape(*tile))
         assert np.array_equal(got.double().cpu().numpy(), want), pol.label
+
+
+@pytest.mark.parametrize("m,n,k,tile", [
+    (1, 4096, 4096, (128, 128, 128)),     # decode-like: partials hold one 32-row chunk
+    (16, 1096, 2048, (128, 128, 64)),     # skinny M with a last column tile over half full
+    (33, 4136, 1024, (128, 128, 128)),    # N % 128 = 40: last column tile skips chunks
+    (20, 600, 4096, (256, 256, 128)),     # CTA pair: rank-1 half entirely past M
+])
+def test_skinny_and_narrow_edge_tiles_bitwise_every_policy(m, n, k, tile):
+    """Stream-K partials and reduction bands bounded to the valid 32-row / 32-column chunks
+    (GemmParams.ragged) stay bitwise equal to the float64 oracle on integer inputs."""
+    _bitwise_every_policy(m, n, k, *tile)

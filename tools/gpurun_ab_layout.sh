@@ -1,0 +1,7 @@
+# A/B the working tree against the build in _orig/ (SKPP_PKG_ROOT)
+for root in _orig2 _orig; do
+  echo "== ${root:-new}"
+  SKPP_PKG_ROOT=$root python tools/launch_modes.py 512 512 16384 ask 128x128x128 | grep "pdl=1"
+  SKPP_PKG_ROOT=$root python tools/launch_modes.py 1 4096 4096 hybrid1 128x128x128 | grep "pdl=1"
+  SKPP_PKG_ROOT=$root python tools/launch_modes.py 1000 1000 1000 hybrid1 128x128x128 | grep "pdl=1"
+done

@@ -6,6 +6,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("SKPP_PKG_ROOT"):  # A/B against another build of the package
+    sys.path.insert(0, os.environ["SKPP_PKG_ROOT"])
 
 
 def main():

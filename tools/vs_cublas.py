@@ -1,0 +1,72 @@
+#!/usr/bin/env python
+"""Context, not a claim: the Stream-K++ kernel next to cuBLAS (torch.matmul) on the same
+shapes, bf16/fp16 in -> bf16/fp16 out (torch.matmul's output type), both timed the way
+bench.py times: K back-to-back launches over rotating operand sets larger than L2.
+
+Our side picks the best measured (tile, policy) per shape from the candidate tiles, i.e.
+what the Bloom-selected config converges to on tuned sizes.  cuBLAS is a library GEMM
+with its own heuristics (split-K, stream-K-like decompositions), not the reference's path.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+TILES = ["128x128x64", "128x64x128", "128x128x128", "256x128x128", "256x256x128"]
+SHAPES = [(1024, 1024, 1024, "fp16"), (512, 512, 16384, "bf16"), (8192, 8192, 8192, "bf16"),
+          (16, 4096, 4096, "bf16"), (128, 4096, 4096, "bf16"), (512, 14336, 4096, "bf16"),
+          (2048, 4096, 4096, "bf16"), (4096, 14336, 4096, "bf16")]
+
+
+def rotate_time_us(fns, steps):
+    import torch
+
+    for f in fns * 2:
+        f()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        fns[i % len(fns)]()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / steps
+
+
+def main():
+    import torch
+
+    import paper_2408_11417_b200 as sk
+    from paper_2408_11417_b200 import sweep, tiles as tl
+
+    rows = []
+    for m, n, k, dts in SHAPES:
+        dt = torch.bfloat16 if dts == "bf16" else torch.float16
+        size = sk.ProblemSize(m, n, k)
+        set_bytes = 2 * (m * k + k * n) + 2 * m * n
+        sets = max(2, min(32, (512 << 20) // set_bytes))
+        ops = [(torch.randn(m, k, device="cuda").to(dt), torch.randn(k, n, device="cuda").to(dt),
+                torch.empty(m, n, device="cuda", dtype=dt)) for _ in range(sets)]
+        flops = 2.0 * m * n * k
+        steps = max(sets, int(min(2000, max(20, 0.3e6 / (flops / 1e12 / 1000 * 1e6 + 5)))) // sets * sets)
+        # ours: best (tile, policy) measured with graph replays, then timed like bench.py
+        pool = sweep.OperandPool([size], dt, dt)
+        per_tile = sweep.measure_size_tiles(size, [tl.parse_tile(t) for t in TILES], sk.canonical_policies(),
+                                            sweep.MeasureParams(warmup=3, reps=5, in_dtype=dt, out_dtype=dt),
+                                            pool, rounds=3)
+        rec = tl.joint_winner(size, per_tile)
+        tile, pol = rec.winner
+        plans = [sk.GemmPlan(a, b, c, pol, tile) for a, b, c in ops]
+        ours = rotate_time_us([p.launch for p in plans], steps)
+        cub = rotate_time_us([(lambda a=a, b=b, c=c: torch.matmul(a, b, out=c)) for a, b, c in ops], steps)
+        row = {"m": m, "n": n, "k": k, "dtype": dts, "ours": f"{tl.tile_label(tile)}/{pol.label}",
+               "ours_us": round(ours, 2), "cublas_us": round(cub, 2),
+               "ours_tflops": round(flops / ours / 1e6, 1), "cublas_tflops": round(flops / cub / 1e6, 1),
+               "speedup_vs_cublas": round(cub / ours, 3)}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+
+
+if __name__ == "__main__":
+    main()
