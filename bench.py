@@ -190,7 +190,7 @@ def ncu_traffic(workload: str, tile_label: str, policy_label: str):
 
 def sweep_summary():
     """Selection quality over the paper grid from the committed GPU sweep run (separate job)."""
-    path = os.path.join(ROOT, "profiles", "round1", "sweep_joint4_summary.json")
+    path = os.path.join(ROOT, "profiles", "round1", "sweep_joint5_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)

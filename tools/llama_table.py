@@ -11,9 +11,9 @@ import paper_2408_11417_b200 as sk  # noqa: E402
 from paper_2408_11417_b200 import tiles as tl  # noqa: E402
 
 R = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "round1")
-TILES = [sk.TileShape(128, 128, 64), sk.TileShape(128, 128, 128), sk.TileShape(256, 256, 64),
-         sk.TileShape(256, 256, 128)]
-paths = [(t, os.path.join(R, f"sweep_joint4_records.{tl.tile_label(t)}.csv")) for t in TILES]
+TILES = [sk.TileShape(128, 128, 64), sk.TileShape(128, 64, 128), sk.TileShape(128, 128, 128),
+         sk.TileShape(256, 256, 64), sk.TileShape(256, 256, 128)]
+paths = [(t, os.path.join(R, f"sweep_joint5_records.{tl.tile_label(t)}.csv")) for t in TILES]
 joint = {r.size: r for r in tl.joint_records_from_csvs(paths)}
 bank = tl.build_tile_bank(list(joint.values()), TILES)
 print("| M | N | dp_util (128x128) | DP 128x128x64 µs | best DP (any tile) µs | selected (tile, policy) | selected µs | TFLOP/s "

@@ -13,11 +13,13 @@ def main():
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import sweep
 
-    sizes = [sk.ProblemSize(*v) for v in [(8192, 2048, 32), (8192, 1024, 512), (1024, 1024, 1024),
-                                          (8192, 2048, 65536), (8192, 8192, 65536), (64, 64, 64)]]
+    spec = os.environ.get("SIZES", "8192x2048x32,8192x1024x512,1024x1024x1024,4x4096x1024,64x64x64")
+    sizes = [sk.ProblemSize(*(int(v) for v in z.split("x"))) for z in spec.split(",")]
+    tiles = [sk.TileShape(*(int(v) for v in t.split("x")))
+             for t in os.environ.get("TILES", "128x128x128,256x256x128").split(",")]
     params = sweep.MeasureParams(warmup=3, reps=10)
     pool = sweep.OperandPool(sizes, params.in_dtype, params.out_dtype)
-    for tile in (sk.TileShape(128, 128, 128), sk.TileShape(256, 256, 128)):
+    for tile in tiles:
         g = sk.executor.default_g(tile)
         for size in sizes:
             ts = []
