@@ -412,6 +412,7 @@ struct GemmParams {
   uint64_t* timeline;  // debug: TL_EVENTS %globaltimer stamps per CTA, or null
   uint32_t b3d;         // tmB is the 3-D (n64, k, chunk) map: one B load per stage
   uint32_t a3d;         // tmA is the 3-D (k64, row, chunk) map: one A load per BK=128 stage
+  uint32_t a_tx;        // A bytes per stage per CTA (the A box covers round_up(M, 8) rows when M < 128)
   uint32_t l2_prefetch; // k-blocks of the first item prefetched to L2 before griddepcontrol.wait
   uint32_t l2_hints;    // B loads evict_last, C stores evict_first (skpp_set_l2_hints)
   uint32_t debug;       // skpp_set_debug: bit 0 = always take the two-pass (owner-late) fixup path
@@ -769,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // the MMA-issuing (rank-0) CTA's barrier expects the bytes of the whole pair
         if (rank == 0)
-          mbar_arrive_expect_tx(&full_bar[stage], CG * (load_a ? C::A_BYTES : C::B_BYTES));
+          mbar_arrive_expect_tx(&full_bar[stage], CG * (load_a ? p.a_tx : C::B_BYTES));
         const int32_t k0 = (int32_t)(kk * BK);
         if constexpr (CG == 1) {
           if (load_a) {
@@ -1531,7 +1532,12 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   // BK = 128 with K % 64 == 0: A as (k in chunk, row, 64-deep chunk) so one 3-D box fills
   // both sub-tiles [chunk][128 rows][64] (the per-SM TMA stage rate falls with fewer ops).
   // Otherwise a chunk could run past a row end, so two 2-D boxes per stage.
-  const bool a3d = g_a3d && BK > 64 && p->k % 64 == 0;
+  // M < 128: the A box covers only round_up(M, 8) rows (a decode-like M = 1 box would be
+  // 99% out of bounds, and TMA's OOB fill is far from free: M = 1 x 14336 x 4096 ran 1.6x
+  // slower than M = 128).  The tile's other rows of shared memory keep stale data, so the
+  // MMA produces junk there — in accumulator rows >= M, which are never stored or reduced.
+  const uint32_t a_rows = p->m < (uint64_t)kBM ? (uint32_t)((p->m + 7) / 8 * 8) : (uint32_t)kBM;
+  const bool a3d = g_a3d && BK > 64 && p->k % 64 == 0 && a_rows == (uint32_t)kBM;
   if (a3d) {
     auto fn = encode_fn();
     const cuuint64_t dims[3] = {64, p->m, p->k / 64};
@@ -1547,7 +1553,7 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
       rc = SKPP_ELAUNCH;
     }
   } else {
-    rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK > 64 ? 64 : BK, kBM, aswz);
+    rc = make_map(&pl->ma, ops->a, in_dt, 2, p->k, p->m, (uint64_t)ops->lda, BK > 64 ? 64 : BK, a_rows, aswz);
   }
   const uint32_t bnc = t->blk_n / (t->blk_m / kBM);  // B columns per CTA
   const bool b3d = g_b3d && p->n % 64 == 0 && bnc > 64;
@@ -1585,6 +1591,7 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   gp.out_dtype = ops->out_dtype;
   gp.b3d = b3d ? 1 : 0;
   gp.a3d = a3d ? 1 : 0;
+  gp.a_tx = a_rows * BK * 2;
   gp.l2_prefetch = (uint32_t)g_l2_prefetch;
   gp.l2_hints = g_l2_hints ? 1 : 0;
   gp.debug = (uint32_t)g_debug;
