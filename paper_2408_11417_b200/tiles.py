@@ -174,6 +174,66 @@ def evaluate_selection(bank: TileBank, records: list[JointRecord], tolerance: fl
     }
 
 
+class Selector:
+    """Stream-K++ selection at run time: Bloom-pruned candidates, measured once per size.
+
+    ``config(size)`` returns the (tile, policy) to run: the candidates of
+    ``bank.candidates(size, nearest)`` (the filters' answer plus the baseline); a single
+    candidate is used directly, several are timed once on the device with ``timer`` and the
+    fastest is cached for the size — the paper's "evaluate only the policies the filters
+    did not eliminate", lifted to (tile, policy).  ``gemm`` runs C = A @ B
+    with the selected configuration.
+    """
+
+    def __init__(self, bank: TileBank, nearest: bool = True, timer=None):
+        self.bank = bank
+        self.nearest = nearest
+        self.timer = timer  # timer(size, [(tile, policy), ...], a, b, out) -> [us, ...]
+        self.cache: dict = {}
+        self.measured = 0   # sizes that needed a measurement (more than one candidate)
+
+    def config(self, size: ProblemSize, a=None, b=None, out=None) -> Config:
+        key = (size.m, size.n, size.k, getattr(a, "dtype", None), getattr(out, "dtype", None))
+        cfg = self.cache.get(key)
+        if cfg is not None:
+            return cfg
+        cand = self.bank.candidates(size, self.nearest)
+        if len(cand) == 1:
+            cfg = cand[0]
+        else:
+            times = (self.timer or _device_timer)(size, cand, a, b, out)
+            self.measured += 1
+            cfg = min(zip(times, range(len(cand)), cand))[2]
+        self.cache[key] = cfg
+        return cfg
+
+    def gemm(self, a, b, out=None, out_dtype=None):
+        import torch
+
+        from .executor import GemmPlan
+
+        if out is None:
+            out = torch.empty((a.shape[0], b.shape[1]), dtype=out_dtype or torch.float32, device=a.device)
+        size = ProblemSize(a.shape[0], b.shape[1], a.shape[1])
+        tile, policy = self.config(size, a, b, out)
+        return GemmPlan(a, b, out, policy, tile).launch()
+
+
+def _device_timer(size, cand, a, b, out):
+    """Median device time (us) of each candidate on the caller's operands (graph replays)."""
+    import torch
+
+    from .executor import GemmPlan
+    from .sweep import MeasureParams, time_plan
+
+    if a is None or b is None:
+        raise ValueError("measuring candidates needs the operands")
+    if out is None:
+        out = torch.empty((size.m, size.n), dtype=torch.float32, device=a.device)
+    params = MeasureParams(warmup=2, reps=5, max_inner=16, target_us=100.0)
+    return [time_plan(GemmPlan(a, b, out, pol, tile), params) for tile, pol in cand]
+
+
 def joint_records_from_csvs(paths_by_tile: list[tuple[TileShape, str]]) -> list[JointRecord]:
     """Rebuild joint records from per-tile records CSVs (reference schema)."""
     from .pipeline import read_records_csv, records_from_rows
@@ -192,6 +252,6 @@ def joint_records_from_csvs(paths_by_tile: list[tuple[TileShape, str]]) -> list[
 
 
 __all__ = [
-    "JointRecord", "TileBank", "build_tile_bank", "evaluate_selection", "joint_records_from_csvs",
+    "JointRecord", "Selector", "TileBank", "build_tile_bank", "evaluate_selection", "joint_records_from_csvs",
     "joint_winner", "parse_tile", "snap_pow2", "tile_label", "CostEstimate", "TuneRecord", "rank_costs",
 ]

@@ -197,3 +197,30 @@ def test_device_schedule_trace_kernel_matches_host():
             lo, hi = int(offsets[x]), int(offsets[x + 1])
             assert cn[x] == hi - lo
             assert np.array_equal(tr[x, : hi - lo], items[lo:hi])
+
+
+@pytest.mark.gpu
+def test_selector_measures_candidates_and_runs_the_selected_config():
+    """tiles.Selector on the device: Bloom candidates timed once, result bitwise vs the oracle."""
+    import numpy as np
+    import torch
+
+    import paper_2408_11417_b200 as sk
+    from oracle import gemm as ogemm
+    from paper_2408_11417_b200 import tiles as tl
+
+    t0, t1 = sk.TileShape(128, 128, 64), sk.TileShape(128, 128, 128)
+    bank = tl.TileBank([t0, t1])
+    size = sk.ProblemSize(512, 384, 2048)
+    bank.insert(size, (t1, sk.Policy.all_stream_k()))
+    rng = np.random.default_rng(5)
+    a = ogemm.random_int_matrix(size.m, size.k, rng)
+    b = ogemm.random_int_matrix(size.k, size.n, rng)
+    at = torch.from_numpy(a).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(b).to(torch.bfloat16).cuda()
+    sel = tl.Selector(bank)
+    c = sel.gemm(at, bt)
+    torch.cuda.synchronize()
+    assert sel.measured == 1 and len(sel.cache) == 1
+    assert sel.config(size, at, bt, c) in bank.candidates(size)
+    assert np.array_equal(c.double().cpu().numpy(), ogemm.reference_gemm(a, b))

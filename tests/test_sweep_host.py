@@ -185,3 +185,29 @@ def test_joint_records_from_per_tile_csvs(tmp_path):
         paths.append((t, str(path)))
     back = tl.joint_records_from_csvs(paths)
     assert [(r.size, r.winner) for r in back] == [(r.size, r.winner) for r in sorted(joint, key=lambda r: (r.size.m, r.size.n, r.size.k))]
+
+
+def test_selector_prunes_with_the_bank_and_caches():
+    """tiles.Selector: one candidate -> no measurement; several -> timed once, fastest cached."""
+    from paper_2408_11417_b200 import tiles as tl
+
+    t0, t1 = sk.TileShape(128, 128, 64), sk.TileShape(256, 256, 128)
+    bank = tl.TileBank([t0, t1])
+    tuned = sk.ProblemSize(1024, 1024, 1024)
+    bank.insert(tuned, (t1, sk.Policy.hybrid(1)))
+    calls = []
+
+    def timer(size, cand, a, b, out):
+        calls.append((size, list(cand)))
+        return [5.0 if c == (t1, sk.Policy.hybrid(1)) else 9.0 for c in cand]
+
+    sel = tl.Selector(bank, nearest=True, timer=timer)
+    # tuned size: filters answer (t1, hybrid1) + baseline (t0, DP) -> measured once
+    assert sel.config(tuned) == (t1, sk.Policy.hybrid(1))
+    assert sel.config(tuned) == (t1, sk.Policy.hybrid(1))
+    assert len(calls) == 1 and sel.measured == 1
+    # an off-grid size snaps to the nearest tuned power of two (1000 -> 1024)
+    assert sel.config(sk.ProblemSize(1000, 1000, 1000)) == (t1, sk.Policy.hybrid(1))
+    # a size nobody tuned: only the baseline is left, no measurement
+    assert sel.config(sk.ProblemSize(3, 5, 7)) == (t0, sk.Policy.data_parallel())
+    assert len(calls) == 2
