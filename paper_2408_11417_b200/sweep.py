@@ -78,12 +78,23 @@ def _pad8(v: int) -> int:
     return (v + 7) // 8 * 8
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(device: int) -> torch.cuda.Stream:
+    """One capture stream per device, reused by every measurement (creating a stream per
+    measurement was a visible share of a sweep's host time)."""
+    st = _SIDE_STREAMS.get(device)
+    if st is None:
+        st = _SIDE_STREAMS[device] = torch.cuda.Stream(device=device)
+    return st
+
+
 def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None) -> float:
     """Median per-launch device time (microseconds) of a prepared GEMM."""
     stream = torch.cuda.current_stream()
     for _ in range(params.warmup):
         plan.launch()
-    torch.cuda.synchronize()
     if est_us is None:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -97,7 +108,7 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
     reps = int(min(params.reps, max(3, math.ceil(20000.0 / (inner * est_us)))))
     if params.use_graphs:
         graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream()
+        side = _side_stream(stream.device_index)
         side.wait_stream(stream)
         with torch.cuda.stream(side):
             with torch.cuda.graph(graph, stream=side):
@@ -110,16 +121,17 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
         def run():
             for _ in range(inner):
                 plan.launch()
-    torch.cuda.synchronize()
-    times = []
+    # all replays queued back to back, one event pair each, a single sync at the end
+    events = []
     for _ in range(reps):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         run()
         e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1) * 1e3 / inner)
+        events.append((e0, e1))
+    events[-1][1].synchronize()
+    times = [e0.elapsed_time(e1) * 1e3 / inner for e0, e1 in events]
     times.sort()
     return times[len(times) // 2]
 
