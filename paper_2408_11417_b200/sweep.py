@@ -93,7 +93,7 @@ def _side_stream(device: int) -> torch.cuda.Stream:
 def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None) -> float:
     """Median per-launch device time (microseconds) of a prepared GEMM."""
     stream = torch.cuda.current_stream()
-    for _ in range(params.warmup):
+    if params.warmup:
         plan.launch()
     if est_us is None:
         t0 = torch.cuda.Event(enable_timing=True)
@@ -103,6 +103,11 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
         t1.record(stream)
         t1.synchronize()
         est_us = max(t0.elapsed_time(t1) * 1e3, 1.0)
+    # the remaining warm-up launches only matter for short kernels: a launch of
+    # >= 0.5 ms is its own warm-up (caches and clocks settle within it)
+    if est_us < 500.0:
+        for _ in range(params.warmup - 1):
+            plan.launch()
     inner = int(max(1, min(params.max_inner, params.target_us // est_us)))
     # big problems: fewer replays (keep ~20 ms of timed work per schedule, >= 3 samples)
     reps = int(min(params.reps, max(3, math.ceil(20000.0 / (inner * est_us)))))
@@ -116,7 +121,8 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
                     plan.launch()
         stream.wait_stream(side)
         run = graph.replay
-        graph.replay()
+        if inner > 1 or est_us < 500.0:
+            graph.replay()  # first replay of a fresh graph carries upload cost
     else:
         def run():
             for _ in range(inner):
