@@ -229,6 +229,27 @@ def roofline(flops: float, nbytes: float, seconds: float, peaks: dict, sustained
             "peak_source": peaks["source"] + ", copy bandwidth"}
 
 
+def fixup_summary(plan, tile, flops: float, nbytes: float, seconds: float) -> dict:
+    """Stream-K partial-tile traffic of one launch (reported beside the roofline).
+
+    Every partial item (owner and peers) writes its 128 x blk_n fp32 accumulator per CTA row
+    half once and the reducers read it back once, so bytes = 2 x items x blk_m x blk_n x 4 —
+    an upper bound when the last row / column tile is ragged (valid chunks only)."""
+    from paper_2408_11417_b200.scheduler import count_partials
+
+    partial, full, peers = count_partials(plan.sched_c)
+    per_item = tile.blk_m * tile.blk_n * 4
+    written = partial * per_item
+    return {
+        "partial_items": partial, "non_owner_partials": peers, "full_tile_stores": full,
+        "bytes_written": written, "bytes_read": written,
+        "vs_algorithmic_bytes": round(2 * written / nbytes, 3),
+        "avg_rate_over_step_gbs": round(2 * written / seconds / 1e9, 1),
+        "note": "partials live in L2 within a launch (ncu DRAM bytes ~= algorithmic); their cost is "
+                "the SM store port (<= 60 GB/s per SM) and the ~7 TB/s chip L2 write rate",
+    }
+
+
 def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool, max_seconds: float,
                     max_reps: int, seed: int = 0):
     """Time the oracle port of the reference executor (float64) on this host."""
@@ -469,6 +490,7 @@ def run_ours(args, wl: dict) -> None:
                 "note": "per-(tile, policy) times from CUDA-graph replays with warm L2 (selection sweep)",
             },
             "roofline": roof,
+            "fixup": fixup_summary(plan, tile, flops, nbytes, per_step_s),
             "sweep": sweep_summary(),
             "cpu_baseline": {
                 "value": round(cpu_value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",

@@ -32,7 +32,7 @@ from dataclasses import dataclass
 import torch
 
 from .costmodel import CostEstimate, TuneRecord, rank_costs
-from .executor import GemmPlan, default_g
+from .executor import GemmPlan, default_g, workspace_for
 from .scheduler import count_partials, schedule_signature
 from .types import Policy, ProblemSize, TileShape, canonical_policies
 
@@ -112,13 +112,23 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
     # big problems: fewer replays (keep ~20 ms of timed work per schedule, >= 3 samples)
     reps = int(min(params.reps, max(3, math.ceil(20000.0 / (inner * est_us)))))
     if params.use_graphs:
+        # Raw capture: torch.cuda.graph() would synchronise, gc.collect() and empty_cache()
+        # before every capture — ~5 ms per measurement, the largest host cost of a
+        # multi-tile sweep.  The plan's fixup workspace for the capture
+        # stream is created here, outside the capture, so the graph allocates nothing.
+        dev = stream.device_index
         graph = torch.cuda.CUDAGraph()
-        side = _side_stream(stream.device_index)
+        side = _side_stream(dev)
+        if plan.ws_bytes:
+            workspace_for(plan.ws_bytes, dev, side.cuda_stream)
         side.wait_stream(stream)
         with torch.cuda.stream(side):
-            with torch.cuda.graph(graph, stream=side):
+            graph.capture_begin()
+            try:
                 for _ in range(inner):
                     plan.launch()
+            finally:
+                graph.capture_end()
         stream.wait_stream(side)
         run = graph.replay
         if inner > 1 or est_us < 500.0:
