@@ -18,6 +18,6 @@ cap() {  # name m n k policy tile dtype
 cap cfg2_128x128x128_hybrid1 512 512 16384 hybrid1 128x128x128 bf16
 cap cfg2_128x128x64_hybrid1 512 512 16384 hybrid1 128x128x64 bf16
 cap cfg1_128x128x128_dp 1024 1024 1024 dp 128x128x128 fp16
-cap cfg1_128x128x64_dp 1024 1024 1024 dp 128x128x64 fp16
+cap cfg1_128x64x128_dp 1024 1024 1024 dp 128x64x128 fp16
 cap square8192_256x256x64_dp 8192 8192 8192 dp 256x256x64 bf16
 cap square8192_256x256x128_dp 8192 8192 8192 dp 256x256x128 bf16
