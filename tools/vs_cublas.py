@@ -14,9 +14,11 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 TILES = ["128x128x64", "128x64x128", "128x128x128", "256x128x128", "256x256x128"]
-SHAPES = [(1024, 1024, 1024, "fp16"), (512, 512, 16384, "bf16"), (8192, 8192, 8192, "bf16"),
+SHAPES = [tuple(int(v) if i < 3 else v for i, v in enumerate(z.split("x"))) for z in
+          os.environ["SHAPES"].split(",")] if os.environ.get("SHAPES") else [(1024, 1024, 1024, "fp16"), (512, 512, 16384, "bf16"), (8192, 8192, 8192, "bf16"),
           (16, 4096, 4096, "bf16"), (128, 4096, 4096, "bf16"), (512, 14336, 4096, "bf16"),
           (2048, 4096, 4096, "bf16"), (4096, 14336, 4096, "bf16")]
+TILES = os.environ.get("TILES", ",".join(TILES)).split(",")
 
 
 def rotate_time_us(fns, steps):
