@@ -223,3 +223,19 @@ def test_skinny_and_narrow_edge_tiles_bitwise_every_policy(m, n, k, tile):
     """Stream-K partials and reduction bands bounded to the valid 32-row / 32-column chunks
     (GemmParams.ragged) stay bitwise equal to the float64 oracle on integer inputs."""
     _bitwise_every_policy(m, n, k, *tile)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (1, 8, 8), (7, 9, 5), (1, 4096, 8), (300, 1, 700), (2, 3, 70000)])
+@pytest.mark.parametrize("tile", [(128, 128, 64), (128, 64, 128), (128, 128, 128), (256, 256, 128)])
+def test_degenerate_shapes_bitwise(m, n, k, tile):
+    """Tiny / degenerate extents (K, N below a TMA box, M = 1, very long K) through the
+    padding host path: bitwise vs the float64 oracle for DP and all-Stream-K."""
+    sk = _sk()
+    a, b = _int_case(m, n, k, seed=m * 31 + n * 7 + k)
+    want = ogemm.reference_gemm(a, b)
+    size, t = sk.ProblemSize(m, n, k), sk.TileShape(*tile)
+    g = sk.executor.default_g(t)
+    for pol in (sk.Policy.data_parallel(), sk.Policy.all_stream_k()):
+        sched = sk.build_schedule(size, t, sk.HardwareModel(g, 1), pol)
+        got = sk.execute_schedule(a, b, sched, t, size)
+        assert np.array_equal(got, want), (pol.label, float(np.abs(got - want).max()))
