@@ -20,6 +20,7 @@ def main() -> None:
     ap.add_argument("--tile", default="128x128x64")
     ap.add_argument("--policy", default="ask")
     ap.add_argument("--flush", action="store_true")
+    ap.add_argument("--out", default="fp32", help="fp32 | bf16")
     ap.add_argument("--per-cta", type=int, default=0, help="print the first N CTAs")
     ap.add_argument("--kstamps", type=int, default=0, help="print CTA 0's first N k-block stamps")
     args = ap.parse_args()
@@ -36,7 +37,8 @@ def main() -> None:
     tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
     a = torch.randn(args.m, args.k, device="cuda").to(torch.bfloat16)
     b = torch.randn(args.k, args.n, device="cuda").to(torch.bfloat16)
-    c = torch.empty(args.m, args.n, device="cuda")
+    c = torch.empty(args.m, args.n, device="cuda",
+                    dtype=torch.bfloat16 if args.out == "bf16" else torch.float32)
     plan = sk.GemmPlan(a, b, c, parse_policy(sk, args.policy), tile)
     grid = plan.g * (tile.blk_m // 128)
     tl = torch.zeros(grid * 16 + 512, dtype=torch.int64, device="cuda")
