@@ -541,6 +541,7 @@ def main(argv=None) -> int:
             jh, _ = merge_tiles(args.out, world, tiles, "heldout")
             summary["selection_offgrid_baseline_fallback"] = evaluate_selection(tb, jh, nearest=False)
             summary["selection_offgrid_nearest_pow2"] = evaluate_selection(tb, jh, nearest=True)
+            summary["selection_offgrid_pow2_corners"] = evaluate_selection(tb, jh, nearest="corners")
         with open(os.path.join(args.out, "summary.json"), "w") as fh:
             json.dump(summary, fh, indent=1)
         print(json.dumps(summary))

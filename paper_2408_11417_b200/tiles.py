@@ -88,16 +88,26 @@ class TileBank:
         tile, pol = cfg
         self.banks[self.tiles.index(tile)].insert(size, pol)
 
-    def query(self, size: ProblemSize, nearest: bool = False) -> list[Config]:
-        """(tile, policy) candidates reported by the filters, tile-major."""
+    def query(self, size: ProblemSize, nearest=False) -> list[Config]:
+        """(tile, policy) candidates reported by the filters, tile-major.
+
+        For a size absent from every filter: ``nearest=True`` (or ``"pow2"``) asks the
+        filters about the nearest power-of-two size; ``nearest="corners"`` takes the union
+        of their answers over the (up to 8) power-of-two sizes enclosing it.
+        """
         out = [(t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(size)]
-        if not out and nearest:
-            snapped = snap_pow2(size)
-            if snapped != size:
-                out = [(t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(snapped)]
+        if out or not nearest:
+            return out
+        probes = snap_corners(size) if nearest == "corners" else [snap_pow2(size)]
+        for z in probes:
+            if z == size:
+                continue
+            for c in ((t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(z)):
+                if c not in out:
+                    out.append(c)
         return out
 
-    def candidates(self, size: ProblemSize, nearest: bool = False) -> list[Config]:
+    def candidates(self, size: ProblemSize, nearest=False) -> list[Config]:
         cand = self.query(size, nearest)
         if self.baseline not in cand:
             cand.append(self.baseline)
@@ -130,6 +140,15 @@ def snap_pow2(size: ProblemSize) -> ProblemSize:
     return ProblemSize(snap(size.m), snap(size.n), snap(size.k))
 
 
+def snap_corners(size: ProblemSize) -> list[ProblemSize]:
+    """The power-of-two sizes enclosing ``size`` (floor / ceil per dimension, deduplicated)."""
+    def both(v: int) -> list[int]:
+        lo = 1 << max(0, int(math.floor(math.log2(v))))
+        return [lo] if lo == v else [lo, lo * 2]
+
+    return [ProblemSize(m, n, k) for m in both(size.m) for n in both(size.n) for k in both(size.k)]
+
+
 def build_tile_bank(records: list[JointRecord], tiles: list[TileShape], **bank_kwargs) -> TileBank:
     """Insert every size's joint winner, in (m, n, k) order (bytes independent of sweep order)."""
     tb = TileBank(tiles, **bank_kwargs)
@@ -139,7 +158,7 @@ def build_tile_bank(records: list[JointRecord], tiles: list[TileShape], **bank_k
 
 
 def evaluate_selection(bank: TileBank, records: list[JointRecord], tolerance: float = 0.2,
-                       nearest: bool = False) -> dict:
+                       nearest=False) -> dict:
     """Selected = fastest measured candidate of bank.candidates(size); compare to the measured oracle.
 
     ``records`` may come from a different measurement run than the one the bank
@@ -178,14 +197,15 @@ class Selector:
     """Stream-K++ selection at run time: Bloom-pruned candidates, measured once per size.
 
     ``config(size)`` returns the (tile, policy) to run: the candidates of
-    ``bank.candidates(size, nearest)`` (the filters' answer plus the baseline); a single
+    ``bank.candidates(size, nearest)`` (the filters' answer plus the baseline; a size the
+    filters never saw takes the union over its enclosing power-of-two sizes); a single
     candidate is used directly, several are timed once on the device with ``timer`` and the
     fastest is cached for the size — the paper's "evaluate only the policies the filters
     did not eliminate", lifted to (tile, policy).  ``gemm`` runs C = A @ B
     with the selected configuration.
     """
 
-    def __init__(self, bank: TileBank, nearest: bool = True, timer=None):
+    def __init__(self, bank: TileBank, nearest="corners", timer=None):
         self.bank = bank
         self.nearest = nearest
         self.timer = timer  # timer(size, [(tile, policy), ...], a, b, out) -> [us, ...]
@@ -253,5 +273,5 @@ def joint_records_from_csvs(paths_by_tile: list[tuple[TileShape, str]]) -> list[
 
 __all__ = [
     "JointRecord", "Selector", "TileBank", "build_tile_bank", "evaluate_selection", "joint_records_from_csvs",
-    "joint_winner", "parse_tile", "snap_pow2", "tile_label", "CostEstimate", "TuneRecord", "rank_costs",
+    "joint_winner", "parse_tile", "snap_corners", "snap_pow2", "tile_label", "CostEstimate", "TuneRecord", "rank_costs",
 ]

@@ -206,8 +206,22 @@ def test_selector_prunes_with_the_bank_and_caches():
     assert sel.config(tuned) == (t1, sk.Policy.hybrid(1))
     assert sel.config(tuned) == (t1, sk.Policy.hybrid(1))
     assert len(calls) == 1 and sel.measured == 1
-    # an off-grid size snaps to the nearest tuned power of two (1000 -> 1024)
+    # an off-grid size takes the filters' answers at its enclosing powers of two (1000 -> 512/1024)
     assert sel.config(sk.ProblemSize(1000, 1000, 1000)) == (t1, sk.Policy.hybrid(1))
     # a size nobody tuned: only the baseline is left, no measurement
     assert sel.config(sk.ProblemSize(3, 5, 7)) == (t0, sk.Policy.data_parallel())
     assert len(calls) == 2
+
+
+def test_snap_corners_encloses_the_size():
+    from paper_2408_11417_b200 import tiles as tl
+
+    z = sk.ProblemSize(1000, 64, 3)
+    corners = tl.snap_corners(z)
+    assert sorted((c.m, c.n, c.k) for c in corners) == [(512, 64, 2), (512, 64, 4), (1024, 64, 2), (1024, 64, 4)]
+    assert tl.snap_corners(sk.ProblemSize(8, 8, 8)) == [sk.ProblemSize(8, 8, 8)]
+    t0 = sk.TileShape(128, 128, 64)
+    bank = tl.TileBank([t0])
+    bank.insert(sk.ProblemSize(512, 64, 4), (t0, sk.Policy.hybrid(2)))
+    assert (t0, sk.Policy.hybrid(2)) in bank.candidates(z, nearest="corners")
+    assert bank.candidates(z, nearest=False) == [bank.baseline]
