@@ -301,3 +301,28 @@ def test_dp_utilization():
     assert sk.dp_utilization(sk.GridInfo(1, 105, 1, 105, 105), 104) == pytest.approx(105 / 208)
     with pytest.raises(ValueError):
         sk.dp_utilization(sk.GridInfo(0, 0, 1, 0, 0), 104)
+
+
+def test_bloom_fp_calibration_like_reference_acceptance():
+    """Reference acceptance criterion (tests/test_acceptance.py:128-155): measured false-positive
+    rate in [0.005, 0.015] at the design load (10,000 members, fp 0.01) over 100,000 guaranteed
+    non-members, and <= 2 / 100,000 at the paper's 923-member load."""
+    import numpy as np
+
+    from paper_2408_11417_b200 import BloomFilter, ProblemSize, encode_key
+
+    rng = np.random.default_rng(77)
+    members = rng.integers(1, 2**40, size=(10_000, 3), dtype=np.uint64)
+    probes = rng.integers(2**40, 2**41, size=(100_000, 3), dtype=np.uint64)
+    keys = [encode_key(ProblemSize(int(m), int(n), int(k))) for m, n, k in probes]
+
+    design = BloomFilter.for_capacity(10_000, 0.01, seed=42)
+    for m, n, k in members:
+        design.insert(encode_key(ProblemSize(int(m), int(n), int(k))))
+    rate = sum(key in design for key in keys) / len(keys)
+    assert 0.005 <= rate <= 0.015, rate
+
+    paper = BloomFilter.for_capacity(10_000, 0.01, seed=43)
+    for m, n, k in members[:923]:
+        paper.insert(encode_key(ProblemSize(int(m), int(n), int(k))))
+    assert sum(key in paper for key in keys) <= 2
