@@ -91,6 +91,12 @@ int skpp_sched_count(const skpp_sched_t* s, uint64_t* total, uint64_t* counts /*
 /* Materialise every workgroup's ordered items, workgroup-major, into rows of
    SKPP_TRACE_FIELDS int64; `offsets` gets g+1 prefix offsets (in items). */
 int skpp_sched_items(const skpp_sched_t* s, int64_t* items, uint64_t cap, uint64_t* offsets);
+/* The schedule as the reference's per-workgroup item lists (scheduler.py:226-254
+   build_schedule): out[(x*max_items + i)*5 + {0..4}] = (tile, local_iter_begin,
+   local_iter_end, write_mode 0=full 1=atomic-partial, phase 0=stream-k 1=data-parallel),
+   counts[x] = items of workgroup x; SKPP_ECAPACITY if a workgroup has more than max_items. */
+int skpp_schedule_trace(const skpp_problem_t* p, const skpp_tile_t* t, uint32_t g,
+                        const skpp_policy_t* pol, uint32_t max_items, int32_t* out, int32_t* counts);
 /* Exactly-once audit by interval sweep over items given as flat [start,end) iteration
    intervals (tile*ipt+kb, tile*ipt+ke).  Writes duplicates and gaps. */
 int skpp_validate_intervals(const uint64_t* starts, const uint64_t* ends, uint64_t n_items,

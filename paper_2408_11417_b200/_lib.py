@@ -88,6 +88,8 @@ SIGNATURES = {
     "skpp_last_error": (C.c_char_p, []),
     "skpp_version": (C.c_char_p, []),
     "skpp_sched_make": (C.c_int, [_P(Problem), _P(Tile), C.c_uint32, _P(PolicyC), _P(SchedC)]),
+    "skpp_schedule_trace": (C.c_int, [_P(Problem), _P(Tile), C.c_uint32, _P(PolicyC), C.c_uint32,
+                                      C.c_void_p, C.c_void_p]),
     "skpp_sched_count": (C.c_int, [_P(SchedC), _u64p, _u64p]),
     "skpp_sched_items": (C.c_int, [_P(SchedC), _i64p, C.c_uint64, _u64p]),
     "skpp_validate_intervals": (

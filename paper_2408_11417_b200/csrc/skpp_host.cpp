@@ -288,6 +288,49 @@ extern "C" int skpp_sched_count(const skpp_sched_t* cs, uint64_t* total, uint64_
   return SKPP_OK;
 }
 
+// SURVEY 8(b) trace contract: per workgroup x < g, up to max_items rows of five int32
+// (tile, local_iter_begin, local_iter_end, write_mode 0=full 1=atomic-partial, phase
+// 0=stream-k 1=data-parallel) at out[(x*max_items + i)*5], item count in counts[x] —
+// the reference's Schedule.assignments (scheduler.py:226-254) flattened.  Host-side decode
+// of the same closed form the kernel walks.
+extern "C" int skpp_schedule_trace(const skpp_problem_t* p, const skpp_tile_t* t, uint32_t g,
+                                   const skpp_policy_t* pol, uint32_t max_items, int32_t* out,
+                                   int32_t* counts) {
+  if (!p || !t || !pol || !out || !counts) {
+    set_error("null argument");
+    return SKPP_EINVAL;
+  }
+  skpp_sched_t cs;
+  int rc = skpp_sched_make(p, t, g, pol, &cs);
+  if (rc) return rc;
+  const Sched s = to_sched(cs);
+  for (uint32_t x = 0; x < s.g; ++x) {
+    Cursor c;
+    cursor_init(c, s, x);
+    Item it;
+    uint32_t n = 0;
+    while (cursor_next(c, s, x, it)) {
+      if (n >= max_items) {
+        set_error("max_items too small for workgroup " + std::to_string(x));
+        return SKPP_ECAPACITY;
+      }
+      if (it.tile > 0x7fffffffull || it.ke > 0x7fffffffull) {
+        set_error("schedule value exceeds int32; use skpp_sched_items");
+        return SKPP_EINVAL;
+      }
+      int32_t* r = out + ((uint64_t)x * max_items + n) * 5;
+      r[0] = (int32_t)it.tile;
+      r[1] = (int32_t)it.kb;
+      r[2] = (int32_t)it.ke;
+      r[3] = it.role == ROLE_FULL ? 0 : 1;
+      r[4] = (int32_t)it.phase;
+      ++n;
+    }
+    counts[x] = (int32_t)n;
+  }
+  return SKPP_OK;
+}
+
 extern "C" int skpp_sched_items(const skpp_sched_t* cs, int64_t* items, uint64_t cap,
                                 uint64_t* offsets) {
   if (!cs || !items || !offsets) {

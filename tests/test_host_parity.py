@@ -380,3 +380,35 @@ def test_query_latency_budget_like_reference_acceptance():
     assert native_ns < 2_000.0, native_ns
     stats = pl.measure_query_latency(bank, sizes, repeat=100_000, warmup=10_000)
     assert stats.median_ns < 10_000.0, stats
+
+
+def test_c_abi_schedule_trace_matches_oracle():
+    """skpp_schedule_trace (SURVEY 8(b) contract: int32 rows (tile, kb, ke, write_mode,
+    phase) per workgroup) equals the oracle's build_schedule item lists."""
+    import ctypes
+
+    import numpy as np
+
+    from oracle import schedule as osched
+    from paper_2408_11417_b200 import _lib
+
+    kinds = {"data-parallel": 0, "hybrid": 1, "all-streamk": 2}
+    rng = np.random.default_rng(8)
+    for _ in range(60):
+        m, n, k = (int(2 ** rng.uniform(0, 12)) for _ in range(3))
+        bm, bn, bk = (int(rng.choice([16, 64, 128, 256])), int(rng.choice([16, 64, 128, 256])),
+                      int(rng.choice([8, 32, 64])))
+        g = int(rng.integers(1, 300))
+        kind = ["data-parallel", "hybrid", "all-streamk"][int(rng.integers(0, 3))]
+        s_b = int(rng.integers(1, 8)) if kind == "hybrid" else 0
+        first = bool(rng.integers(0, 2)) if kind == "hybrid" else True
+        want = osched.build_schedule(m, n, k, bm, bn, bk, g, kind, s_b, first)
+        cap = max(1, max(len(w) for w in want))
+        out = np.zeros((g, cap, 5), dtype=np.int32)
+        counts = np.zeros(g, dtype=np.int32)
+        rc = _lib.lib.skpp_schedule_trace(ctypes.byref(_lib.Problem(m, n, k)), ctypes.byref(_lib.Tile(bm, bn, bk)),
+                                          g, ctypes.byref(_lib.PolicyC(kinds[kind], s_b, int(first))), cap,
+                                          out.ctypes.data, counts.ctypes.data)
+        assert rc == 0
+        got = [[tuple(int(v) for v in out[x, i]) for i in range(counts[x])] for x in range(g)]
+        assert got == [[tuple(r) for r in w] for w in want], (m, n, k, bm, bn, bk, g, kind, s_b, first)
