@@ -20,6 +20,8 @@ def main():
         _lib.lib.skpp_set_l2_prefetch(int(os.environ["SKPP_PF"]))
     if os.environ.get("SKPP_A3D"):
         _lib.lib.skpp_set_a3d(int(os.environ["SKPP_A3D"]))
+    if os.environ.get("SKPP_DEBUG"):
+        _lib.lib.skpp_set_debug(int(os.environ["SKPP_DEBUG"]))
     if os.environ.get("SKPP_L2_HINTS"):
         _lib.lib.skpp_set_l2_hints(int(os.environ["SKPP_L2_HINTS"]))
     from tools.profile_gemm import parse_policy
