@@ -405,6 +405,9 @@ enum : int {
   TL_PART_FLAG = 10,  // first partial: flag released
   TL_SUM1 = 11,       // phase 2: first summation pass done (thread 128)
   TL_SUM2 = 12,       // phase 2: owner pass done (only when the owner was late)
+  TL_BS0 = 13,        // band_sum (first pass, thread 128): clock64 at entry,
+  TL_BS1 = 14,        //   after its first batch of partial loads returned,
+  TL_BS2 = 15,        //   and at exit (SM cycles, not ns)
   TL_EVENTS = 16
 };
 __device__ __forceinline__ uint64_t gtimer() {
@@ -483,6 +486,7 @@ struct ReduceArgs {
   uint64_t x0;         // first contributing workgroup
   uint32_t rank;       // row half (CTA rank in the pair)
   uint32_t nc;         // contributors
+  uint64_t* tl;        // debug timeline row of this CTA, or null
 };
 
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t epoch) {
@@ -520,7 +524,10 @@ __device__ __noinline__ void band_sum(const float4* __restrict__ wsv, uint64_t s
                                       uint32_t peer_slot_step, uint64_t owner_slot, uint32_t nc,
                                       uint32_t R0, uint32_t nrows, uint32_t V, uint32_t sstride,
                                       uint32_t term_begin, uint32_t term_end, uint32_t accumulate,
-                                      uint32_t stage, uint32_t ft) {
+                                      uint32_t stage, uint32_t ft, uint64_t* tl) {
+  const bool stamp = tl != nullptr && ft == kEpiWarp0 * 32 && term_begin == 0;
+  if (stamp) tl[TL_BS0] = clock64();
+  bool first = true;
   const uint32_t total = nrows * V;
   for (uint32_t e0 = ft; e0 < total; e0 += G * kThreads) {
     float4 acc[G];
@@ -551,6 +558,10 @@ __device__ __noinline__ void band_sum(const float4* __restrict__ wsv, uint64_t s
         if (t0 + b < term_end) {
 #pragma unroll
           for (int g = 0; g < G; ++g) {
+            if (stamp && first && b == 0 && g == 0) {
+              tl[TL_BS1] = clock64() + (q[0][0].x == 12345.f ? 1 : 0);  // after the first load returned
+              first = false;
+            }
             acc[g].x += q[g][b].x;
             acc[g].y += q[g][b].y;
             acc[g].z += q[g][b].z;
@@ -563,6 +574,7 @@ __device__ __noinline__ void band_sum(const float4* __restrict__ wsv, uint64_t s
     for (int g = 0; g < G; ++g)
       if (e0 + g * kThreads < total) st_shared_f4(saddr[g], acc[g]);
   }
+  if (stamp) tl[TL_BS2] = clock64();
 }
 
 // Store the reduced band: consecutive threads take consecutive column groups of
@@ -591,10 +603,10 @@ __device__ __forceinline__ void band_reduce(const ReduceArgs& ra, uint32_t R0, u
   const uint64_t peer0 = 2 * ((ra.x0 + 1) * CG + ra.rank);
   if (ra.nc <= 4)
     band_sum<4, 4>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, SV + 1, term_begin, term_end,
-                   accumulate, stage, ft);
+                   accumulate, stage, ft, ra.tl);
   else
     band_sum<2, 12>(ra.wsv, ra.slot_v, peer0, 2 * CG, ra.slot0, ra.nc, R0, nrows, V, SV + 1, term_begin, term_end,
-                    accumulate, stage, ft);
+                    accumulate, stage, ft, ra.tl);
 }
 
 // Hand an accumulator stage back to the MMA issuer (the rank-0 CTA's barrier).
@@ -1059,7 +1071,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t tile = s.dp_tiles + u;
       const uint64_t row0 = (tile / s.n_tiles) * TILE_M + rank * kBM + R0;
       const uint64_t gcol0 = (tile % s.n_tiles) * BN;
-      const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc};
+      const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc,
+                          p.timeline ? p.timeline + (uint64_t)blockIdx.x * TL_EVENTS : nullptr};
       const uint32_t stage = smem_u32(smem);  // idle operand ring: float4 [row][V+1]
       // Peer flags are awaited by one thread each; thread kThreads-1 polls the
       // owner's flag until either it is up or every peer has been seen.

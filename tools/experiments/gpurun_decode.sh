@@ -1,4 +1,11 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests rc=$?; tail -3 gpurun_out/gpu_tests.log
-for r in 1 2; do for root in _orig ""; do echo "== ${root:-new}"
-for sz in "1 14336 4096 dp 128x128x128" "16 4096 4096 hybrid1 128x128x128" "512 512 16384 ask 128x128x128" "1024 1024 1024 dp 128x64x128"; do
-  SKPP_PKG_ROOT=$root python tools/launch_modes.py $sz 2>&1 | grep "pdl=1"; done; done; done
+#!/bin/bash
+# Decode-shape (M<=128) breakdown: timelines + launch modes for the candidate tiles.
+cd /root/repo
+mkdir -p gpurun_out/decode
+for m in 16 128; do
+  for cfg in "hybrid1 128x128x128" "hybrid1 128x64x128" "ask 128x64x128" "data-parallel 128x64x128" "hybrid1 128x128x64"; do
+    set -- $cfg
+    timeout 120 python tools/launch_modes.py $m 4096 4096 $1 $2 2>&1 | grep pdl=1 >> gpurun_out/decode/modes.txt
+    timeout 120 python tools/timeline.py --m $m --n 4096 --k 4096 --policy $1 --tile $2 --kstamps 12 >> gpurun_out/decode/timeline.txt 2>&1
+  done
+done

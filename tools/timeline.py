@@ -71,6 +71,12 @@ def main() -> None:
         if len(col):
             print(f"  {name:>10}: min {col.min() / 1e3:8.2f}  med {sorted(col)[len(col) // 2] / 1e3:8.2f}  "
                   f"max {col.max() / 1e3:8.2f} us  (n={len(col)})")
+    bs = t[:, 13:16]
+    ok = (bs[:, 0] > 0) & (bs[:, 1] > 0) & (bs[:, 2] > 0)
+    if ok.any():
+        lat, tot = bs[ok, 1] - bs[ok, 0], bs[ok, 2] - bs[ok, 0]
+        print(f"  band_sum (thread 128, SM cycles): first loads back med {sorted(lat)[len(lat) // 2]:.0f} "
+              f"max {lat.max():.0f}; whole pass med {sorted(tot)[len(tot) // 2]:.0f} max {tot.max():.0f}  (n={ok.sum()})")
     if args.kstamps:
         n = int((ks[:, 1] > 0).sum())
         c0 = ks[0, 0]
