@@ -239,3 +239,46 @@ def test_degenerate_shapes_bitwise(m, n, k, tile):
         sched = sk.build_schedule(size, t, sk.HardwareModel(g, 1), pol)
         got = sk.execute_schedule(a, b, sched, t, size)
         assert np.array_equal(got, want), (pol.label, float(np.abs(got - want).max()))
+
+
+# Seeded fuzz over the whole device surface: random shapes (M arbitrary, N and K
+# multiples of 8 as TMA needs), every implemented tile, canonical and non-canonical
+# policies (hybrid s up to 9, DP-first), random grid sizes.  Each case is checked
+# bitwise against the float64 oracle and its device item trace against the oracle's
+# build_schedule, so any schedule/fixup disagreement shows up as a named case.
+_FUZZ_TILES = [(128, bn, bk) for bn in (64, 128, 256) for bk in (16, 32, 64, 128)] + \
+              [(256, bn, bk) for bn in (128, 256) for bk in (32, 64, 128)]
+
+
+def _fuzz_cases(n_cases=100, seed=2408):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n_cases):
+        tile = _FUZZ_TILES[int(rng.integers(len(_FUZZ_TILES)))]
+        m = int(rng.integers(1, 1400))
+        n = 8 * int(rng.integers(1, 180))
+        k = 8 * int(rng.integers(1, 700))
+        gmax = 148 // (tile[0] // 128)
+        g = int(rng.choice([gmax, gmax, int(rng.integers(1, gmax + 1))]))
+        kind = int(rng.integers(3))
+        pol = ("dp",) if kind == 0 else ("ask",) if kind == 1 else ("hybrid", int(rng.integers(1, 10)), bool(rng.integers(2)))
+        cases.append((i, m, n, k, tile, g, pol))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: f"fuzz{c[0]}-{c[1]}x{c[2]}x{c[3]}-{c[4][0]}x{c[4][1]}x{c[4][2]}-g{c[5]}-{c[6][0]}")
+def test_fuzz_bitwise_and_trace(case):
+    sk = _sk()
+    i, m, n, k, tile, g, pol = case
+    policy = (sk.Policy.data_parallel() if pol[0] == "dp" else sk.Policy.all_stream_k() if pol[0] == "ask"
+              else sk.Policy.hybrid(pol[1], sk_first=pol[2]))
+    a, b = _int_case(m, n, k, seed=1000 + i)
+    got, plan = _run(a, b, policy, sk.TileShape(*tile), g=g, trace_cap=512)
+    want = ogemm.reference_gemm(a, b)
+    gd = got.double().cpu().numpy()
+    assert np.array_equal(gd, want), float(np.nanmax(np.abs(gd - want)))
+    ref = osched.build_schedule(m, n, k, tile[0], tile[1], tile[2], g, policy.kind.value, policy.sk_batches,
+                                policy.sk_first)
+    if max(len(w) for w in ref) <= 512:
+        dev = [[row[:5] for row in wg] for wg in plan.trace_items()]
+        assert dev == ref
