@@ -513,6 +513,14 @@ def main(argv=None) -> int:
     if rank == 0:
         joint, paths = merge_tiles(args.out, world, tiles, "records")
         tb = build_tile_bank(joint, tiles)
+        # calibrated cost model per tile: the prior for sizes the filters never saw
+        from .costmodel import calibrate
+
+        for tile, path in paths:
+            recs = pl.records_from_rows(pl.read_records_csv(path))
+            tb.priors[tiles.index(tile)] = calibrate(
+                ((r.size, [(p, e.makespan) for p, e in r.costs]) for r in recs), tile,
+                default_g(tile))
         tb.save(os.path.join(args.out, "tilebank"))
         times = [json.load(open(os.path.join(args.out, f"timing.rank{r}.json")))["seconds"] for r in range(world)]
         n_pairs = len(sizes) * 7 * len(tiles)
@@ -542,6 +550,8 @@ def main(argv=None) -> int:
             summary["selection_offgrid_baseline_fallback"] = evaluate_selection(tb, jh, nearest=False)
             summary["selection_offgrid_nearest_pow2"] = evaluate_selection(tb, jh, nearest=True)
             summary["selection_offgrid_pow2_corners"] = evaluate_selection(tb, jh, nearest="corners")
+            summary["selection_offgrid_corners_and_model"] = evaluate_selection(tb, jh, nearest="corners+model")
+        summary["costmodel_priors"] = {tile_label(t): c.to_dict() for t, c in zip(tiles, tb.priors)}
         with open(os.path.join(args.out, "summary.json"), "w") as fh:
             json.dump(summary, fh, indent=1)
         print(json.dumps(summary))

@@ -13,7 +13,10 @@ Query: candidates = union over tiles of (tile, p) for p in bank[tile].query(size
 plus the baseline (first tile, data-parallel), which is always evaluated.
 There are no false negatives: the measured winner is always a candidate.
 Sizes absent from every bank fall back to the baseline, or — with
-``nearest=True`` — to the candidates of the nearest tuned power-of-two size.
+``nearest=True`` — to the candidates of the nearest tuned power-of-two size,
+``"corners"`` — the union over the enclosing power-of-two sizes, ``"model"`` — the
+pick of the calibrated cost model (``costmodel.calibrate``, stored per tile in the
+manifest as ``prior``), or ``"corners+model"`` — both.
 """
 
 from __future__ import annotations
@@ -23,7 +26,7 @@ import math
 import os
 from dataclasses import dataclass
 
-from .costmodel import CostEstimate, TuneRecord, rank_costs
+from .costmodel import Calibration, CostEstimate, TuneRecord, rank_costs
 from .sieve import SieveBank
 from .types import Policy, ProblemSize, TileShape
 
@@ -79,6 +82,7 @@ class TileBank:
         if len(self.banks) != len(self.tiles):
             raise ValueError("one bank per tile")
         self._tuned_keys: set | None = None
+        self.priors: list[Calibration | None] = [None] * len(self.tiles)  # per tile, optional
 
     @property
     def baseline(self) -> Config:
@@ -98,14 +102,36 @@ class TileBank:
         out = [(t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(size)]
         if out or not nearest:
             return out
-        probes = snap_corners(size) if nearest == "corners" else [snap_pow2(size)]
-        for z in probes:
-            if z == size:
-                continue
-            for c in ((t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(z)):
-                if c not in out:
-                    out.append(c)
+        if nearest != "model":
+            probes = snap_corners(size) if nearest in ("corners", "corners+model") else [snap_pow2(size)]
+            for z in probes:
+                if z == size:
+                    continue
+                for c in ((t, p) for t, b in zip(self.tiles, self.banks) for p in b.query(z)):
+                    if c not in out:
+                        out.append(c)
+        if nearest in ("model", "corners+model") and any(c is not None for c in self.priors):
+            pick = self.prior_pick(size)
+            if pick not in out:
+                out.append(pick)
         return out
+
+    def prior_pick(self, size: ProblemSize) -> Config:
+        """The (tile, policy) with the lowest calibrated-model time (ties: earlier tile,
+        then the reference tie-break), over the tiles that carry a prior."""
+        from .types import canonical_policies
+
+        best = None
+        for ti, (tile, cal) in enumerate(zip(self.tiles, self.priors)):
+            if cal is None:
+                continue
+            for pol in canonical_policies():
+                key = (cal.predict_us(size, pol), ti, pol.sort_key())
+                if best is None or key < best[0]:
+                    best = (key, (tile, pol))
+        if best is None:
+            raise ValueError("no tile of this bank carries a calibrated cost-model prior")
+        return best[1]
 
     def candidates(self, size: ProblemSize, nearest=False) -> list[Config]:
         cand = self.query(size, nearest)
@@ -116,10 +142,13 @@ class TileBank:
     def save(self, out_dir: str) -> None:
         os.makedirs(out_dir, exist_ok=True)
         manifest = []
-        for t, b in zip(self.tiles, self.banks):
+        for t, b, prior in zip(self.tiles, self.banks, self.priors):
             name = f"bank_{tile_label(t)}.sieve"
             b.save(os.path.join(out_dir, name))
-            manifest.append({"tile": tile_label(t), "bank": name})
+            entry = {"tile": tile_label(t), "bank": name}
+            if prior is not None:
+                entry["prior"] = prior.to_dict()
+            manifest.append(entry)
         with open(os.path.join(out_dir, "tilebank.json"), "w") as fh:
             json.dump({"format": "skpp-tilebank-1", "tiles": manifest}, fh, indent=1)
 
@@ -129,7 +158,9 @@ class TileBank:
             man = json.load(fh)
         tiles = [parse_tile(e["tile"]) for e in man["tiles"]]
         banks = [SieveBank.load(os.path.join(out_dir, e["bank"])) for e in man["tiles"]]
-        return cls(tiles, banks)
+        tb = cls(tiles, banks)
+        tb.priors = [Calibration.from_dict(e["prior"]) if "prior" in e else None for e in man["tiles"]]
+        return tb
 
 
 def snap_pow2(size: ProblemSize) -> ProblemSize:
@@ -198,14 +229,15 @@ class Selector:
 
     ``config(size)`` returns the (tile, policy) to run: the candidates of
     ``bank.candidates(size, nearest)`` (the filters' answer plus the baseline; a size the
-    filters never saw takes the union over its enclosing power-of-two sizes); a single
+    filters never saw takes the union over its enclosing power-of-two sizes and the
+    calibrated cost model's pick, when the bank carries priors); a single
     candidate is used directly, several are timed once on the device with ``timer`` and the
     fastest is cached for the size — the paper's "evaluate only the policies the filters
     did not eliminate", lifted to (tile, policy).  ``gemm`` runs C = A @ B
     with the selected configuration.
     """
 
-    def __init__(self, bank: TileBank, nearest="corners", timer=None):
+    def __init__(self, bank: TileBank, nearest="corners+model", timer=None):
         self.bank = bank
         self.nearest = nearest
         self.timer = timer  # timer(size, [(tile, policy), ...], a, b, out) -> [us, ...]

@@ -224,3 +224,25 @@ def test_selector_measures_candidates_and_runs_the_selected_config():
     assert sel.measured == 1 and len(sel.cache) == 1
     assert sel.config(size, at, bt, c) in bank.candidates(size)
     assert np.array_equal(c.double().cpu().numpy(), ogemm.reference_gemm(a, b))
+
+
+def test_joint_sweep_end_to_end_with_calibrated_priors(tmp_path):
+    """sweep.main over two tiles on a tiny grid: per-tile records, tile bank with a
+    calibrated cost-model prior per tile, and the off-grid selection summaries."""
+    import json
+    import os
+
+    from paper_2408_11417_b200 import sweep
+    from paper_2408_11417_b200 import tiles as tl
+
+    out = str(tmp_path / "sw")
+    rc = sweep.main(["--out", out, "--grid", "small", "--tiles", "128x128x64,128x128x128", "--reps", "2",
+                     "--warmup", "1", "--max-gflop", "0.002", "--heldout", "8"])
+    assert rc == 0
+    summary = json.load(open(os.path.join(out, "summary.json")))
+    assert set(summary["costmodel_priors"]) == {"128x128x64", "128x128x128"}
+    assert "selection_offgrid_corners_and_model" in summary
+    bank = tl.TileBank.load(os.path.join(out, "tilebank"))
+    assert all(p is not None for p in bank.priors)
+    size = sk().ProblemSize(3000, 5000, 7000)
+    assert bank.prior_pick(size) in bank.query(size, nearest="corners+model")
