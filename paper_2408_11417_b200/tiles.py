@@ -121,6 +121,10 @@ class TileBank:
         then the reference tie-break), over the tiles that carry a prior."""
         from .types import canonical_policies
 
+        ckey = (size.m, size.n, size.k, tuple(id(c) for c in self.priors))
+        cache = self.__dict__.setdefault("_prior_cache", {})
+        if ckey in cache:
+            return cache[ckey]
         best = None
         for ti, (tile, cal) in enumerate(zip(self.tiles, self.priors)):
             if cal is None:
@@ -131,6 +135,9 @@ class TileBank:
                     best = (key, (tile, pol))
         if best is None:
             raise ValueError("no tile of this bank carries a calibrated cost-model prior")
+        if len(cache) > 65536:
+            cache.clear()
+        cache[ckey] = best[1]
         return best[1]
 
     def candidates(self, size: ProblemSize, nearest=False) -> list[Config]:

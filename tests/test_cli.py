@@ -80,3 +80,14 @@ def test_tune_tiny_grid_and_verify_on_gpu(tmp_path):
             assert row.policy in bank.query(row.size)
     assert cli.main(["verify", "--cases", "35", "--seed", "3"]) == 0
     assert cli.main(["verify", "--cases", "8", "--seed", "3", "--inject-fault"]) == 1
+
+
+def test_query_tile_bank_with_cost_model_prior(capsys):
+    import os
+
+    bank_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "round1", "tilebank5")
+    assert cli.main(["query", "--sieve", bank_dir, "--size", "3000x5000x7000", "--repeat", "10"]) == 0
+    out = capsys.readouterr().out
+    assert "cost-model prior:" in out and "candidates for 3000x5000x7000:" in out
+    assert cli.main(["query", "--sieve", bank_dir, "--size", "512x512x16384", "--nearest", "none", "--repeat", "10"]) == 0
+    assert "128x128x128/" in capsys.readouterr().out
