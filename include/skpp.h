@@ -154,6 +154,13 @@ void skpp_set_a3d(int enable);
 /* k-blocks of each workgroup's first item to prefetch into L2 before the kernel waits on
    the previous grid (PDL); 0 disables (plans created after the call). */
 void skpp_set_l2_prefetch(int k_blocks);
+/* Order in which tile indices map to C tiles (plans created after the call).  0: the
+   reference's row-major order (locate_iter, scheduler.py:155-165).  G > 0: bands of G
+   tile rows walked column by column, so the tiles running concurrently share A and B
+   blocks in L2.  -1 (default): G = 16 (8 when K >= 8192) for grids of >= 4 waves of
+   tiles, row-major otherwise.  The schedule (which workgroup runs which tile index and
+   k-range) is the reference's either way; only the index -> C-region map changes. */
+void skpp_set_raster(int rows);
 /* L2 cache-policy hints on the operand stream (default on; plans created after the call):
    B k-blocks are loaded evict_last (the next wave of tiles re-reads them), C tiles are
    stored evict_first. */

@@ -132,6 +132,7 @@ SIGNATURES = {
     "skpp_set_b3d": (None, [C.c_int]),
     "skpp_set_a3d": (None, [C.c_int]),
     "skpp_set_l2_prefetch": (None, [C.c_int]),
+    "skpp_set_raster": (None, [C.c_int]),
     "skpp_set_l2_hints": (None, [C.c_int]),
     "skpp_set_debug": (None, [C.c_int]),
     "skpp_device_info": (C.c_int, [C.c_int, _P(C.c_int32), _P(C.c_int32), _P(C.c_int32)]),
