@@ -197,13 +197,17 @@ def sweep_summary():
     except (OSError, ValueError):
         return None
     held = d.get("selection_heldout_run", {})
-    off = d.get("selection_offgrid_nearest_pow2", {})
+    off = d.get("selection_offgrid_corners_and_model") or d.get("selection_offgrid_pow2_corners", {})
+    pow2 = d.get("selection_offgrid_nearest_pow2", {})
     return {
         "source": os.path.relpath(path, ROOT) + " (separate sweep job on the same GPU pool)",
         "sizes": d.get("sizes"),
         "tiles": d.get("tiles"),
         "pct_within_20pct_of_oracle_heldout_run": round(100 * held.get("fraction_within", float("nan")), 2),
         "pct_within_20pct_of_oracle_offgrid_sizes": round(100 * off.get("fraction_within", float("nan")), 2),
+        "offgrid_fallback": "union of the filters at the enclosing power-of-two sizes + calibrated cost-model pick"
+        if "selection_offgrid_corners_and_model" in d else "union of the filters at the enclosing power-of-two sizes",
+        "pct_within_20pct_offgrid_nearest_pow2_only": round(100 * pow2.get("fraction_within", float("nan")), 2),
         "eliminated_fraction": held.get("eliminated_fraction"),
         "shape_policy_per_s_1gpu": round(d.get("shape_policy_per_s", 0.0), 1),
     }

@@ -24,6 +24,7 @@ Replaces the analytic ``tune_grid`` loop of the reference
 
 from __future__ import annotations
 
+import dataclasses
 import heapq
 import math
 import time
@@ -49,6 +50,7 @@ class MeasureParams:
     out_dtype: torch.dtype = torch.float32
     peak_tflops: float = DENSE_BF16_PEAK_TFLOPS
     use_graphs: bool = True
+    timed_us: float = 20000.0  # timed work per schedule for big problems (>= 3 samples)
 
 
 class OperandPool:
@@ -109,8 +111,8 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
         for _ in range(params.warmup - 1):
             plan.launch()
     inner = int(max(1, min(params.max_inner, params.target_us // est_us)))
-    # big problems: fewer replays (keep ~20 ms of timed work per schedule, >= 3 samples)
-    reps = int(min(params.reps, max(3, math.ceil(20000.0 / (inner * est_us)))))
+    # big problems: fewer replays (keep ~timed_us of timed work per schedule, >= 3 samples)
+    reps = int(min(params.reps, max(3, math.ceil(params.timed_us / (inner * est_us)))))
     if params.use_graphs:
         # Raw capture: torch.cuda.graph() would synchronise, gc.collect() and empty_cache()
         # before every capture — ~5 ms per measurement, the largest host cost of a
@@ -167,8 +169,8 @@ def measure_size(
     the first few schedules of such a size came out up to 1.6x slower than the same
     schedules measured later (8192x14336x4096: DP 1231 us vs 763 us for hybrid5, which
     interleaved re-measurement puts within a few %).  They are therefore preceded by a
-    ~30 ms soak of the first schedule and measured in two passes (forward, then reverse
-    order), keeping each schedule's faster pass.
+    ~20 ms soak of the first schedule and measured in two passes of half the timed work
+    (forward, then reverse order), keeping each schedule's faster pass.
     """
     a, b, c = pool.views(size)
     plans: dict[tuple, GemmPlan] = {}
@@ -192,9 +194,10 @@ def measure_size(
     if first_us >= HEAVY_US:
         for _ in range(int(math.ceil(SOAK_US / first_us))):
             first.launch()
+        half = dataclasses.replace(params, timed_us=params.timed_us / 2)  # same total timed work
         for rnd in range(2):
             for sig in (order if rnd == 0 else order[::-1]):
-                us = time_plan(plans[sig], params)
+                us = time_plan(plans[sig], half)
                 times[sig] = min(us, times.get(sig, us))
     else:
         for sig in order:
@@ -215,7 +218,7 @@ def measure_size(
 
 
 HEAVY_US = 200.0   # sizes whose schedules run at the power cap (see measure_size)
-SOAK_US = 30000.0
+SOAK_US = 20000.0
 
 
 def measure_size_tiles(
