@@ -485,18 +485,22 @@ __device__ __forceinline__ void store_vec4(const GemmParams& p, uint64_t row, ui
 // column: a bijection on [0, T) that keeps the ~g tiles running concurrently inside G
 // rows and ~g/G columns, so their A and B blocks stay in L2 instead of every wave
 // streaming all of B from HBM (multi-wave grids only; see skpp_set_raster).
+// RASTER is a template parameter so that the row-major instantiations (every grid below
+// 4 waves) compile to exactly the code they had before the banded order existed; a
+// runtime branch here measured 0.5-1% slower on cfg2 and decode shapes.
+template <bool RASTER>
 __device__ __forceinline__ void tile_rc(const Sched& s, uint32_t raster, uint64_t t, uint64_t& tm, uint64_t& tn) {
-  if (raster == 0) {
+  if constexpr (!RASTER) {
     tm = t / s.n_tiles;
-    tn = t - tm * s.n_tiles;
-    return;
+    tn = t % s.n_tiles;
+  } else {
+    const uint64_t m_tiles = (s.dp_tiles + s.sk_tiles) / s.n_tiles;
+    const uint64_t band_tiles = (uint64_t)raster * s.n_tiles;
+    const uint64_t band = t / band_tiles, r = t - band * band_tiles;
+    const uint64_t rows = m_tiles - band * raster < raster ? m_tiles - band * raster : raster;
+    tm = band * raster + r % rows;
+    tn = r / rows;
   }
-  const uint64_t m_tiles = (s.dp_tiles + s.sk_tiles) / s.n_tiles;
-  const uint64_t band_tiles = (uint64_t)raster * s.n_tiles;
-  const uint64_t band = t / band_tiles, r = t - band * band_tiles;
-  const uint64_t rows = m_tiles - band * raster < raster ? m_tiles - band * raster : raster;
-  tm = band * raster + r % rows;
-  tn = r / rows;
 }
 
 struct ReduceArgs {
@@ -639,7 +643,7 @@ __device__ __forceinline__ void release_acc_t(uint64_t* bar) {
 }
 #define release_acc(bar) release_acc_t<CG>(bar)
 
-template <int BN, int BK, int CG>
+template <int BN, int BK, int CG, bool RASTER = false>
 __global__ void __launch_bounds__(kThreads, 1)
     streamk_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
@@ -714,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Item it0;
     if (cursor_next(c0, s, x, it0)) {
       uint64_t tm0, tn0;
-      tile_rc(s, p.raster, it0.tile, tm0, tn0);
+      tile_rc<RASTER>(s, p.raster, it0.tile, tm0, tn0);
       const int32_t m0 = (int32_t)(tm0 * TILE_M + rank * kBM);
       const int32_t n0 = (int32_t)(tn0 * BN + rank * C::BNC);
       const uint64_t kend = it0.kb + p.l2_prefetch < it0.ke ? it0.kb + p.l2_prefetch : it0.ke;
@@ -755,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Item it;
     while (cursor_next(cur, s, x, it)) {
       uint64_t tm_, tn_;
-      tile_rc(s, p.raster, it.tile, tm_, tn_);
+      tile_rc<RASTER>(s, p.raster, it.tile, tm_, tn_);
       const int32_t m0 = (int32_t)(tm_ * TILE_M + rank * kBM);
       const int32_t n0 = (int32_t)(tn_ * BN + rank * C::BNC);
       // Serpentine K: every other FULL item of this workgroup walks K backwards.  A
@@ -917,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool partial = it.role != ROLE_FULL;
       const uint64_t slot = 2ull * cta + (sk_seen == 0 ? 0 : 1);
       uint64_t tm_, tn_;
-      tile_rc(s, p.raster, it.tile, tm_, tn_);
+      tile_rc<RASTER>(s, p.raster, it.tile, tm_, tn_);
       const uint64_t tile_row0 = tm_ * TILE_M + rank * kBM;
       const uint64_t tile_col0 = tn_ * BN;
       if (partial) {
@@ -1081,7 +1085,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t rows_ok = kBM, Vv = V;
       if (p.ragged) {
         uint64_t utm, utn;
-        tile_rc(s, p.raster, s.dp_tiles + u, utm, utn);
+        tile_rc<RASTER>(s, p.raster, s.dp_tiles + u, utm, utn);
         const uint64_t tile_rows0 = utm * TILE_M + rank * kBM;
         if (tile_rows0 >= p.M)
           rows_ok = 0;  // this row half of the tile is entirely past M: empty band below
@@ -1098,7 +1102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t slot0 = 2 * (x0 * CG + rank) + (aligned ? 0 : 1);
       const uint64_t tile = s.dp_tiles + u;
       uint64_t ttm, ttn;
-      tile_rc(s, p.raster, tile, ttm, ttn);
+      tile_rc<RASTER>(s, p.raster, tile, ttm, ttn);
       const uint64_t row0 = ttm * TILE_M + rank * kBM + R0;
       const uint64_t gcol0 = ttn * BN;
       const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc,
@@ -1264,23 +1268,23 @@ struct Plan {
   void* ws_bound;   // workspace the parameters point into
 };
 
-template <int BN, int BK, int CG>
+template <int BN, int BK, int CG, bool RASTER = false>
 static int kernel_setup(const void** func, uint32_t* smem) {
   using C = Cfg<BN, BK, CG>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK, CG>,
+    err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK, CG, RASTER>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (err == cudaSuccess && CG == 2)
-      err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK, CG>,
+      err = cudaFuncSetAttribute(streamk_gemm_kernel<BN, BK, CG, RASTER>,
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   });
   if (err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
     return SKPP_ELAUNCH;
   }
-  *func = reinterpret_cast<const void*>(streamk_gemm_kernel<BN, BK, CG>);
+  *func = reinterpret_cast<const void*>(streamk_gemm_kernel<BN, BK, CG, RASTER>);
   *smem = C::SMEM;
   return SKPP_OK;
 }
@@ -1618,6 +1622,16 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   } else {
     const uint64_t T = gp.s.dp_tiles + gp.s.sk_tiles;
     gp.raster = T >= 4ull * pl->cs.g ? (p->k >= 8192 ? 8u : 16u) : 0u;
+  }
+  if (gp.raster) {
+    rc = dispatch_tile(t, [&](auto bn, auto bk, auto cg) {
+      return kernel_setup<decltype(bn)::value, decltype(bk)::value, decltype(cg)::value, true>(&pl->func,
+                                                                                            &pl->smem);
+    });
+    if (rc) {
+      delete pl;
+      return rc;
+    }
   }
   gp.l2_hints = g_l2_hints ? 1 : 0;
   gp.debug = (uint32_t)g_debug;
