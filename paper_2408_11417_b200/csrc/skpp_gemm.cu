@@ -930,14 +930,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // and a contributor's share of columns is one contiguous range.
         float4* dst = reinterpret_cast<float4*>(p.ws + slot * (uint64_t)(kBM * BN)) + row;
         // Only rows < M and columns < N are ever reduced (phase 2 bounds its bands the same
-        // way, at 32-row / 32-column granularity), so the partial of a ragged or skinny
-        // tile (decode-like M = 1..127) costs only its valid chunks on the SM's store port.
-        // Warp-uniform: a warp skips its 32 rows when they are all past M, and every warp
-        // skips the 32-column chunks past N.
+        // way: exact rows, 32-column chunks), so the partial of a ragged or skinny tile
+        // (decode-like M = 1..127) costs only its valid rows and chunks on the SM's store
+        // port.  A warp skips its TMEM reads when all its 32 rows are past M; threads skip
+        // the stores of rows past M; every warp skips the 32-column chunks past N.
         const bool warp_rows_ok = tile_row0 + ew * 32 < p.M;
+        const bool warp_rows_all = tile_row0 + ew * 32 + 32 <= p.M;
+        const bool row_ok = tile_row0 + row < p.M;
         const uint64_t cols_left = p.N - tile_col0;
         const int chunks_ok = cols_left >= (uint64_t)BN ? BN / 32 : (int)((cols_left + 31) / 32);
-        if (!p.ragged || (warp_rows_ok && chunks_ok == BN / 32)) {  // full tile: every row and column chunk
+        if (!p.ragged || (warp_rows_all && chunks_ok == BN / 32)) {  // full tile: every row and column chunk
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             uint32_t w[32];
@@ -962,7 +964,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmem_ld_wait();
 #pragma unroll
               for (int j = 0; j < 8; ++j)
-                dst[(c * 8 + j) * kBM] = make_float4(__uint_as_float(w[4 * j]), __uint_as_float(w[4 * j + 1]),
+                if (row_ok)
+                  dst[(c * 8 + j) * kBM] = make_float4(__uint_as_float(w[4 * j]), __uint_as_float(w[4 * j + 1]),
                                                      __uint_as_float(w[4 * j + 2]), __uint_as_float(w[4 * j + 3]));
             }
             if (c == BN / 32 - 1) {
@@ -1090,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tile_rows0 >= p.M)
           rows_ok = 0;  // this row half of the tile is entirely past M: empty band below
         else if (p.M - tile_rows0 < (uint64_t)kBM)
-          rows_ok = (uint32_t)((p.M - tile_rows0 + 31) / 32 * 32);
+          rows_ok = (uint32_t)(p.M - tile_rows0);  // exact: phase 1 wrote rows < M only
         const uint64_t tile_cols0 = utn * BN;
         if (p.N - tile_cols0 < (uint64_t)BN) Vv = (uint32_t)((p.N - tile_cols0 + 31) / 32 * 32 / 4);
       }
