@@ -177,11 +177,12 @@ def ncu_traffic(workload: str, tile_label: str, policy_label: str):
     capture is of a different kernel configuration than the one this run selected."""
     path = os.path.join(ROOT, "profiles", f"ncu_bench_{workload}.json")
     bm, bn, bk = (int(v) for v in tile_label.split("x"))
-    want = f"<{bn}, {bk}, {bm // 128}>"
+    want = f"<{bn}, {bk}, {bm // 128}"  # template args <BN, BK, CG[, RASTER]>
     try:
         with open(path) as fh:
             rows = json.load(fh)
-        row = next(r for r in rows if "streamk_gemm" in r.get("kernel", "") and want in r["kernel"]
+        row = next(r for r in rows if "streamk_gemm" in r.get("kernel", "")
+                   and (want + ">" in r["kernel"] or want + "," in r["kernel"])
                    and r.get("policy", policy_label) == policy_label)
         return int(row["dram_traffic_bytes"]), os.path.relpath(path, ROOT)
     except (OSError, ValueError, KeyError, StopIteration):
