@@ -7,6 +7,8 @@ and every fixup order.  Random-normal inputs are checked against a float64
 product of the same rounded operands with the tolerance stated per test.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -266,7 +268,7 @@ def _fuzz_cases(n_cases=100, seed=2408):
     return cases
 
 
-@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: f"fuzz{c[0]}-{c[1]}x{c[2]}x{c[3]}-{c[4][0]}x{c[4][1]}x{c[4][2]}-g{c[5]}-{c[6][0]}")
+@pytest.mark.parametrize("case", _fuzz_cases(int(os.environ.get("SKPP_FUZZ_CASES", "100"))), ids=lambda c: f"fuzz{c[0]}-{c[1]}x{c[2]}x{c[3]}-{c[4][0]}x{c[4][1]}x{c[4][2]}-g{c[5]}-{c[6][0]}")
 def test_fuzz_bitwise_and_trace(case):
     sk = _sk()
     i, m, n, k, tile, g, pol = case
