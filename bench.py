@@ -287,10 +287,21 @@ def run_reference(args, wl: dict) -> None:
     cores = len(os.sched_getaffinity(0))
     m, n, k = wl["m"], wl["n"], wl["k"]
     flops = 2.0 * m * n * k
-    # The reference ranks policies with its cost model; for T < g every
-    # Stream-K policy ties and the ordinal tie-break credits hybrid1.
-    pol = ("hybrid", 1, True)
-    wl = dict(wl, tile=wl.get("tile", (128, 128, 64)))  # the reference's executor cost barely depends on it
+    # Same (tile, policy) as our arm: the configuration its selection picked in the committed
+    # bench line of this workload (the reference executor's cost barely depends on it);
+    # otherwise hybrid1 on 128x128x64 (for T < g every Stream-K policy ties and the
+    # reference's ordinal tie-break credits hybrid1).
+    pol, tile = ("hybrid", 1, True), (128, 128, 64)
+    try:
+        with open(os.path.join(ROOT, "profiles", "round1", f"bench_{args.workload}.json")) as fh:
+            cfg = json.load(fh)["config"]
+        tile = tuple(int(v) for v in cfg["tile"])
+        lab = cfg["policy"]
+        pol = (("data-parallel", 0, False) if lab == "data-parallel" else ("all-streamk", 0, False)
+               if lab == "all-streamk" else ("hybrid", int(lab[len("hybrid"):].split("-")[0]), "dpfirst" not in lab))
+    except (OSError, ValueError, KeyError):
+        pass
+    wl = dict(wl, tile=tile)
     cpu_oracle_gemm(wl, *pol, max_seconds=30, max_reps=args.warmup)  # warm-up
     # bounded: K steps or 60 s of CPU work, whichever comes first
     times = cpu_oracle_gemm(wl, *pol, max_seconds=60, max_reps=args.steps)
@@ -301,8 +312,9 @@ def run_reference(args, wl: dict) -> None:
         "steps": len(times), "warmup": args.warmup, "ms_per_step": round(total / len(times) * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (integer-valued float64, seed 0)",
-        "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]), "g": 148,
-                   "policy": "hybrid1", "l2": "n/a (CPU)"},
+        "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]),
+                   "g": 148 // (wl["tile"][0] // 128),
+                   "policy": pol[0] if pol[0] != "hybrid" else f"hybrid{pol[1]}", "l2": "n/a (CPU)"},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": f"{len(times)} full {m}x{n}x{k} schedule executions "
