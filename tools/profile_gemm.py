@@ -48,6 +48,8 @@ def main() -> None:
 
     if os.environ.get("SKPP_L2_HINTS"):
         _lib.lib.skpp_set_l2_hints(int(os.environ["SKPP_L2_HINTS"]))
+    if os.environ.get("SKPP_RASTER"):
+        _lib.lib.skpp_set_raster(int(os.environ["SKPP_RASTER"]))
 
     _lib.lib.skpp_set_b3d(args.b3d)
     dt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
