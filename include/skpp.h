@@ -51,11 +51,21 @@ enum { SKPP_DATA_PARALLEL = 0, SKPP_HYBRID = 1, SKPP_ALL_STREAM_K = 2 };
 /* work-item roles recorded in schedule traces */
 enum { SKPP_ROLE_FULL = 0, SKPP_ROLE_OWNER = 1, SKPP_ROLE_PEER = 2 };
 
-/* trace record: one int64[6] row per work item, per CTA (workgroup) */
-#define SKPP_TRACE_FIELDS 6 /* tile, kb, ke, write_mode(0 full,1 partial), phase(0 sk,1 dp), role */
+/* trace record: one int64[8] row per work item, per CTA (workgroup):
+   tile, kb, ke, write_mode (0 full, 1 partial), phase (0 sk, 1 dp), role,
+   tile_m, tile_n (the C tile the item wrote: scheduler.py:155-165 locate_iter when
+   tile_order == 0, the banded map of skpp_tile_t.tile_order otherwise) */
+#define SKPP_TRACE_FIELDS 8
 
 typedef struct { uint64_t m, n, k; } skpp_problem_t;           /* types.py:28-45 ProblemSize  */
-typedef struct { uint32_t blk_m, blk_n, blk_k; } skpp_tile_t;  /* types.py:58-72 TileShape    */
+/* types.py:58-72 TileShape, plus the kernel's tile order (a B200 tuning parameter that is
+   not in the reference): 0 = the reference's row-major tile index -> (tile_m, tile_n) map
+   (scheduler.py:155-165 locate_iter; the parity mode); G > 0 = bands of G tile rows walked
+   column by column (tile t of band b = t / (G*n_tiles), r = t % (G*n_tiles), rows = min(G,
+   m_tiles - b*G): tile_m = b*G + r % rows, tile_n = r / rows), so the tiles running
+   concurrently share A and B blocks in L2.  The schedule (which workgroup runs which tile
+   index and k-range) is the reference's either way; host-only functions ignore the field. */
+typedef struct { uint32_t blk_m, blk_n, blk_k, tile_order; } skpp_tile_t;
 typedef struct { int32_t kind, sk_batches, sk_first; } skpp_policy_t; /* types.py:95-166 Policy */
 
 /* Closed-form geometry of one (problem, tile, g, policy) schedule:
@@ -97,6 +107,10 @@ int skpp_sched_items(const skpp_sched_t* s, int64_t* items, uint64_t cap, uint64
    counts[x] = items of workgroup x; SKPP_ECAPACITY if a workgroup has more than max_items. */
 int skpp_schedule_trace(const skpp_problem_t* p, const skpp_tile_t* t, uint32_t g,
                         const skpp_policy_t* pol, uint32_t max_items, int32_t* out, int32_t* counts);
+/* C tile (tile_m, tile_n) of tile index `tile` under `tile_order` (skpp_tile_t.tile_order;
+   0 = scheduler.py:155-165 locate_iter) — the map the GEMM kernel uses. */
+int skpp_tile_coords(const skpp_sched_t* s, uint32_t tile_order, uint64_t tile, uint64_t* tile_m,
+                     uint64_t* tile_n);
 /* Exactly-once audit by interval sweep over items given as flat [start,end) iteration
    intervals (tile*ipt+kb, tile*ipt+ke).  Writes duplicates and gaps. */
 int skpp_validate_intervals(const uint64_t* starts, const uint64_t* ends, uint64_t n_items,
@@ -154,13 +168,6 @@ void skpp_set_a3d(int enable);
 /* k-blocks of each workgroup's first item to prefetch into L2 before the kernel waits on
    the previous grid (PDL); 0 disables (plans created after the call). */
 void skpp_set_l2_prefetch(int k_blocks);
-/* Order in which tile indices map to C tiles (plans created after the call).  0: the
-   reference's row-major order (locate_iter, scheduler.py:155-165).  G > 0: bands of G
-   tile rows walked column by column, so the tiles running concurrently share A and B
-   blocks in L2.  -1 (default): G = 16 (8 when K >= 8192) for grids of >= 4 waves of
-   tiles, row-major otherwise.  The schedule (which workgroup runs which tile index and
-   k-range) is the reference's either way; only the index -> C-region map changes. */
-void skpp_set_raster(int rows);
 /* L2 cache-policy hints on the operand stream (default on; plans created after the call):
    B k-blocks are loaded evict_last (the next wave of tiles re-reads them), C tiles are
    stored evict_first. */

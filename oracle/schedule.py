@@ -109,3 +109,32 @@ def fixup_roles(schedule, ipt: int):
             roles.append(0 if wm == FULL else (1 if kb == 0 else 2))
         out.append(roles)
     return out
+
+
+def locate_tile(t: int, n_tiles: int):
+    """scheduler.py:155-165 (locate_iter): tile t is C tile (t // n_tiles, t % n_tiles), row-major."""
+    return divmod(t, n_tiles)
+
+
+def banded_order(m_tiles: int, n_tiles: int, band: int):
+    """Not in the reference: the B200 kernel's banded tile order (skpp_tile_t.tile_order,
+    include/skpp.h).  Built by enumeration — bands of ``band`` tile rows from the top, each
+    walked column by column, rows inside a column top to bottom — so it checks the closed
+    form in skpp_sched.h:tile_coords independently.  Returns the list index -> (tile_m, tile_n);
+    ``band == 0`` is the reference's row-major order."""
+    if band == 0:
+        return [locate_tile(t, n_tiles) for t in range(m_tiles * n_tiles)]
+    order = []
+    for r0 in range(0, m_tiles, band):
+        rows = range(r0, min(r0 + band, m_tiles))
+        for tn in range(n_tiles):
+            for tm in rows:
+                order.append((tm, tn))
+    return order
+
+
+def trace_coords(schedule, m_tiles: int, n_tiles: int, band: int = 0):
+    """Per workgroup, the (tile_m, tile_n) each item of ``schedule`` writes under tile order
+    ``band`` (the last two fields of a device trace row)."""
+    order = banded_order(m_tiles, n_tiles, band)
+    return [[order[t] for t, _kb, _ke, _wm, _ph in wg] for wg in schedule]

@@ -20,7 +20,7 @@ ETRUNCATED, EBADMAGIC, EVERSION, EFORMAT, ECHECKSUM = 20, 21, 22, 23, 24
 
 F32, F16, BF16 = 0, 1, 2
 DATA_PARALLEL, HYBRID, ALL_STREAM_K = 0, 1, 2
-TRACE_FIELDS = 6
+TRACE_FIELDS = 8  # tile, kb, ke, write_mode, phase, role, tile_m, tile_n
 
 
 class Problem(C.Structure):
@@ -28,7 +28,12 @@ class Problem(C.Structure):
 
 
 class Tile(C.Structure):
-    _fields_ = [("blk_m", C.c_uint32), ("blk_n", C.c_uint32), ("blk_k", C.c_uint32)]
+    _fields_ = [("blk_m", C.c_uint32), ("blk_n", C.c_uint32), ("blk_k", C.c_uint32), ("tile_order", C.c_uint32)]
+
+
+def tile_c(tile) -> Tile:
+    """skpp_tile_t of a TileShape (tile order 0, the reference's) or a KernelTile."""
+    return Tile(tile.blk_m, tile.blk_n, tile.blk_k, getattr(tile, "band_rows", 0))
 
 
 class PolicyC(C.Structure):
@@ -96,6 +101,7 @@ SIGNATURES = {
         C.c_int,
         [_u64p, _u64p, C.c_uint64, C.c_uint64, _u64p, _u64p],
     ),
+    "skpp_tile_coords": (C.c_int, [_P(SchedC), C.c_uint32, C.c_uint64, _P(C.c_uint64), _P(C.c_uint64)]),
     "skpp_workspace_bytes": (C.c_uint64, [_P(Problem), _P(Tile), C.c_uint32]),
     "skpp_tile_supported": (C.c_int, [_P(Tile)]),
     "skpp_gemm_launch": (
@@ -132,7 +138,6 @@ SIGNATURES = {
     "skpp_set_b3d": (None, [C.c_int]),
     "skpp_set_a3d": (None, [C.c_int]),
     "skpp_set_l2_prefetch": (None, [C.c_int]),
-    "skpp_set_raster": (None, [C.c_int]),
     "skpp_set_l2_hints": (None, [C.c_int]),
     "skpp_set_debug": (None, [C.c_int]),
     "skpp_device_info": (C.c_int, [C.c_int, _P(C.c_int32), _P(C.c_int32), _P(C.c_int32)]),

@@ -428,16 +428,21 @@ constexpr int TL_KSTAMPS = 256;
 #define SKPP_STAMP(p, ev) \
   do { if ((p).timeline) (p).timeline[(uint64_t)blockIdx.x * TL_EVENTS + (ev)] = gtimer(); } while (0)
 
-__device__ __forceinline__ void record_item(const GemmParams& p, uint32_t x, uint64_t idx,
-                                            const Item& it) {
-  if (p.trace == nullptr || idx >= p.trace_cap) return;
-  int64_t* r = p.trace + ((uint64_t)x * p.trace_cap + idx) * SKPP_TRACE_FIELDS;
+// One trace row: the item (tile, kb, ke, write mode, phase, role) and the C tile it wrote.
+__device__ __forceinline__ void write_trace_row(int64_t* r, const Item& it, uint64_t tm, uint64_t tn) {
   r[0] = (int64_t)it.tile;
   r[1] = (int64_t)it.kb;
   r[2] = (int64_t)it.ke;
   r[3] = it.role == ROLE_FULL ? 0 : 1;
   r[4] = (int64_t)it.phase;
   r[5] = (int64_t)it.role;
+  r[6] = (int64_t)tm;
+  r[7] = (int64_t)tn;
+}
+__device__ __forceinline__ void record_item(const GemmParams& p, uint32_t x, uint64_t idx, const Item& it,
+                                            uint64_t tm, uint64_t tn) {
+  if (p.trace == nullptr || idx >= p.trace_cap) return;
+  write_trace_row(p.trace + ((uint64_t)x * p.trace_cap + idx) * SKPP_TRACE_FIELDS, it, tm, tn);
 }
 
 // Direct (non-TMA) store of one packed 128-byte row segment; used only when C
@@ -480,27 +485,13 @@ __device__ __forceinline__ void store_vec4(const GemmParams& p, uint64_t row, ui
   }
 }
 
-// Tile index -> (tile row, tile column).  raster == 0 is the reference's row-major
-// order (scheduler.py:155-165).  raster == G walks bands of G tile rows column by
-// column: a bijection on [0, T) that keeps the ~g tiles running concurrently inside G
-// rows and ~g/G columns, so their A and B blocks stay in L2 instead of every wave
-// streaming all of B from HBM (multi-wave grids only; see skpp_set_raster).
-// RASTER is a template parameter so that the row-major instantiations (every grid below
-// 4 waves) compile to exactly the code they had before the banded order existed; a
-// runtime branch here measured 0.5-1% slower on cfg2 and decode shapes.
+// Tile index -> C tile (skpp_sched.h tile_coords).  RASTER is a template parameter so
+// that the reference-order instantiations (tile_order == 0, the parity mode) compile to the
+// plain row-major division; a runtime branch here measured 0.5-1% slower on cfg2 and
+// decode shapes.
 template <bool RASTER>
 __device__ __forceinline__ void tile_rc(const Sched& s, uint32_t raster, uint64_t t, uint64_t& tm, uint64_t& tn) {
-  if constexpr (!RASTER) {
-    tm = t / s.n_tiles;
-    tn = t % s.n_tiles;
-  } else {
-    const uint64_t m_tiles = (s.dp_tiles + s.sk_tiles) / s.n_tiles;
-    const uint64_t band_tiles = (uint64_t)raster * s.n_tiles;
-    const uint64_t band = t / band_tiles, r = t - band * band_tiles;
-    const uint64_t rows = m_tiles - band * raster < raster ? m_tiles - band * raster : raster;
-    tm = band * raster + r % rows;
-    tn = r / rows;
-  }
+  tile_coords(s, RASTER ? raster : 0u, t, tm, tn);
 }
 
 struct ReduceArgs {
@@ -913,7 +904,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     Item it;
     while (cursor_next(cur, s, x, it)) {
       const uint32_t as = local & 1, aph = (local >> 1) & 1;
-      if (leader && rank == 0) record_item(p, x, local, it);
       mbar_wait(&tfull_bar[as], aph, 4);
       tc_fence_after();
       if (leader && local == 0) SKPP_STAMP(p, TL_EPI_FIRST);
@@ -922,6 +912,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t slot = 2ull * cta + (sk_seen == 0 ? 0 : 1);
       uint64_t tm_, tn_;
       tile_rc<RASTER>(s, p.raster, it.tile, tm_, tn_);
+      if (leader && rank == 0) record_item(p, x, local, it, tm_, tn_);
       const uint64_t tile_row0 = tm_ * TILE_M + rank * kBM;
       const uint64_t tile_col0 = tn_ * BN;
       if (partial) {
@@ -1171,7 +1162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Decode-only: every CTA walks its items with the same cursor and records them.
-__global__ void schedule_trace_kernel(const Sched s, int64_t* trace, uint64_t cap,
+__global__ void schedule_trace_kernel(const Sched s, uint32_t band, int64_t* trace, uint64_t cap,
                                       int64_t* counts) {
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= s.g) return;
@@ -1181,13 +1172,9 @@ __global__ void schedule_trace_kernel(const Sched s, int64_t* trace, uint64_t ca
   uint64_t n = 0;
   while (cursor_next(cur, s, x, it)) {
     if (n < cap) {
-      int64_t* r = trace + ((uint64_t)x * cap + n) * SKPP_TRACE_FIELDS;
-      r[0] = (int64_t)it.tile;
-      r[1] = (int64_t)it.kb;
-      r[2] = (int64_t)it.ke;
-      r[3] = it.role == ROLE_FULL ? 0 : 1;
-      r[4] = (int64_t)it.phase;
-      r[5] = (int64_t)it.role;
+      uint64_t tm, tn;
+      tile_coords(s, band, it.tile, tm, tn);
+      write_trace_row(trace + ((uint64_t)x * cap + n) * SKPP_TRACE_FIELDS, it, tm, tn);
     }
     ++n;
   }
@@ -1254,7 +1241,6 @@ static int g_pdl = 1;                    // skpp_set_pdl
 static int g_b3d = 1;                    // skpp_set_b3d
 static int g_a3d = 1;                    // skpp_set_a3d
 static int g_l2_prefetch = 2;            // skpp_set_l2_prefetch (k-blocks)
-static int g_raster = -1;                // skpp_set_raster: -1 auto, 0 row-major, G > 0 forced
 static int g_l2_hints = 1;               // skpp_set_l2_hints
 static int g_debug = 0;                  // skpp_set_debug
 
@@ -1426,7 +1412,6 @@ extern "C" void skpp_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 extern "C" void skpp_set_b3d(int enable) { g_b3d = enable ? 1 : 0; }
 extern "C" void skpp_set_a3d(int enable) { g_a3d = enable ? 1 : 0; }
 extern "C" void skpp_set_l2_prefetch(int k_blocks) { g_l2_prefetch = k_blocks > 0 ? k_blocks : 0; }
-extern "C" void skpp_set_raster(int rows) { g_raster = rows < 0 ? -1 : rows; }
 extern "C" void skpp_set_l2_hints(int enable) { g_l2_hints = enable ? 1 : 0; }
 extern "C" void skpp_set_debug(int flags) { g_debug = flags; }
 
@@ -1617,15 +1602,10 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   gp.a3d = a3d ? 1 : 0;
   gp.a_tx = a_rows * BK * 2;
   gp.l2_prefetch = (uint32_t)g_l2_prefetch;
-  // Banded tile order for grids of >= 4 waves (measured: +11% on 4096x14336x4096, +4% on
-  // 8192^3; neutral-to-slower below 4 waves, e.g. -2% on 4096^3 and on split-K cfg2).
-  // Narrower bands when K is long (each band's A and B blocks grow with K).
-  if (g_raster >= 0) {
-    gp.raster = (uint32_t)g_raster;
-  } else {
-    const uint64_t T = gp.s.dp_tiles + gp.s.sk_tiles;
-    gp.raster = T >= 4ull * pl->cs.g ? (p->k >= 8192 ? 8u : 16u) : 0u;
-  }
+  // Tile order: a declared tuning parameter of the tile (skpp_tile_t.tile_order), selected
+  // by the sweep like the tile shape; 0 = the reference's row-major order.  Banded orders
+  // measured +11% on 4096x14336x4096 and +4% on 8192^3, neutral-to-slower below 4 waves.
+  gp.raster = t->tile_order;
   if (gp.raster) {
     rc = dispatch_tile(t, [&](auto bn, auto bk, auto cg) {
       return kernel_setup<decltype(bn)::value, decltype(bk)::value, decltype(cg)::value, true>(&pl->func,
@@ -1755,7 +1735,7 @@ extern "C" int skpp_schedule_trace_device(const skpp_problem_t* p, const skpp_ti
   sched_from_c(cs, s);
   const uint32_t threads = 128;
   schedule_trace_kernel<<<(g + threads - 1) / threads, threads, 0,
-                          reinterpret_cast<cudaStream_t>(stream)>>>(s, trace, trace_cap,
+                          reinterpret_cast<cudaStream_t>(stream)>>>(s, t->tile_order, trace, trace_cap,
                                                                      trace_counts);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -356,10 +356,28 @@ extern "C" int skpp_sched_items(const skpp_sched_t* cs, int64_t* items, uint64_t
       r[3] = it.role == ROLE_FULL ? 0 : 1;
       r[4] = (int64_t)it.phase;
       r[5] = (int64_t)it.role;
+      uint64_t tm, tn;
+      tile_coords(s, 0u, it.tile, tm, tn);  // the reference's locate_iter (row-major)
+      r[6] = (int64_t)tm;
+      r[7] = (int64_t)tn;
       ++n;
     }
   }
   offsets[s.g] = n;
+  return SKPP_OK;
+}
+
+extern "C" int skpp_tile_coords(const skpp_sched_t* cs, uint32_t tile_order, uint64_t tile, uint64_t* tile_m,
+                                uint64_t* tile_n) {
+  if (!cs || !tile_m || !tile_n) {
+    set_error("null argument");
+    return SKPP_EINVAL;
+  }
+  if (tile >= cs->total_tiles) {
+    set_error("tile index out of range");
+    return SKPP_EINVAL;
+  }
+  tile_coords(to_sched(*cs), tile_order, tile, *tile_m, *tile_n);
   return SKPP_OK;
 }
 

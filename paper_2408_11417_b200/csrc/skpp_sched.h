@@ -109,4 +109,23 @@ SKPP_HD uint64_t items_of(const Sched& s, uint32_t x) {
   return n;
 }
 
+// Tile index -> (tile row, tile column) of C.  band == 0 is the reference's row-major
+// order (scheduler.py:155-165 locate_iter: tile_m = t / n_tiles, tile_n = t % n_tiles).
+// band == G > 0 (skpp_tile_t.tile_order) walks bands of G tile rows column by column: a
+// bijection on [0, T) that keeps the ~g tiles running concurrently inside G rows and
+// ~g/G columns, so their A and B blocks stay in L2.  The last band has m_tiles % G rows.
+SKPP_HD void tile_coords(const Sched& s, uint32_t band, uint64_t t, uint64_t& tm, uint64_t& tn) {
+  if (band == 0) {
+    tm = t / s.n_tiles;
+    tn = t % s.n_tiles;
+    return;
+  }
+  const uint64_t m_tiles = (s.dp_tiles + s.sk_tiles) / s.n_tiles;
+  const uint64_t band_tiles = (uint64_t)band * s.n_tiles;
+  const uint64_t b = t / band_tiles, r = t - b * band_tiles;
+  const uint64_t rows = m_tiles - b * band < band ? m_tiles - b * band : band;
+  tm = b * band + r % rows;
+  tn = r / rows;
+}
+
 }  // namespace skpp

@@ -121,7 +121,7 @@ def max_coresident(tile: TileShape) -> int:
     _require_cuda()
     n = ctypes.c_int32()
     _lib.check(
-        _lib.lib.skpp_max_coresident(_lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k), ctypes.byref(n))
+        _lib.lib.skpp_max_coresident(_lib.tile_c(tile), ctypes.byref(n))
     )
     return int(n.value)
 
@@ -133,7 +133,7 @@ def default_g(tile: TileShape, device: int | None = None) -> int:
 
 
 def tile_supported(tile: TileShape) -> bool:
-    return bool(_lib.lib.skpp_tile_supported(_lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k)))
+    return bool(_lib.lib.skpp_tile_supported(_lib.tile_c(tile)))
 
 
 def workspace_for(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
@@ -220,7 +220,7 @@ class GemmPlan:
         )
         handle = ctypes.c_void_p()
         rc = _lib.lib.skpp_plan_create(
-            _lib.Problem(m, n, k), _lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k), policy_to_c(policy),
+            _lib.Problem(m, n, k), _lib.tile_c(tile), policy_to_c(policy),
             self.g, ops,
             self.trace.data_ptr() if self.trace is not None else None, self.trace_cap,
             self.trace_counts.data_ptr() if self.trace_counts is not None else None,

@@ -16,6 +16,8 @@ Reference map: ``WriteMode``/``Phase``/``WorkItem``/``Schedule`` 40-92,
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 from enum import Enum
 from typing import NamedTuple
@@ -159,7 +161,7 @@ def closed_form(size: ProblemSize, tile: TileShape, g: int, policy: Policy) -> _
     out = _lib.SchedC()
     rc = _lib.lib.skpp_sched_make(
         _lib.Problem(size.m, size.n, size.k),
-        _lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k),
+        _lib.tile_c(tile),
         g,
         policy_to_c(policy),
         out,
@@ -169,11 +171,20 @@ def closed_form(size: ProblemSize, tile: TileShape, g: int, policy: Policy) -> _
     return out
 
 
+def tile_coords(sched_c: _lib.SchedC, tile_order: int, tile: int) -> tuple[int, int]:
+    """C tile (tile_m, tile_n) the GEMM kernel writes for tile index ``tile`` under
+    ``tile_order`` (0 = the reference's ``locate_iter``, G > 0 = bands of G tile rows)."""
+    tm, tn = ctypes.c_uint64(), ctypes.c_uint64()
+    _lib.check(_lib.lib.skpp_tile_coords(sched_c, tile_order, tile, ctypes.byref(tm), ctypes.byref(tn)))
+    return int(tm.value), int(tn.value)
+
+
 def schedule_arrays(sched_c: _lib.SchedC) -> tuple[np.ndarray, np.ndarray]:
-    """(items[n, 6] int64, offsets[g+1]) of the closed form, workgroup-major.
+    """(items[n, 8] int64, offsets[g+1]) of the closed form, workgroup-major.
 
     Item columns: tile, kb, ke, write_mode (0 full / 1 partial), phase
-    (0 Stream-K / 1 data-parallel), role (0 full / 1 owner / 2 peer).
+    (0 Stream-K / 1 data-parallel), role (0 full / 1 owner / 2 peer), and the
+    C tile (tile_m, tile_n) of the reference's row-major ``locate_iter``.
     """
     total = np.zeros(1, dtype=np.uint64)
     _lib.check(_lib.lib.skpp_sched_count(sched_c, total.ctypes.data_as(_lib._u64p), None))

@@ -28,17 +28,21 @@ from dataclasses import dataclass
 
 from .costmodel import Calibration, CostEstimate, TuneRecord, rank_costs
 from .sieve import SieveBank
-from .types import Policy, ProblemSize, TileShape
+from .types import Policy, ProblemSize, TileShape, kernel_tile, tile_order
 
 Config = tuple  # (TileShape, Policy)
 
 
 def tile_label(t: TileShape) -> str:
-    return f"{t.blk_m}x{t.blk_n}x{t.blk_k}"
+    """``MxNxK`` for the reference's tile order, ``MxNxKbG`` for G-row bands (KernelTile)."""
+    band = tile_order(t)
+    return f"{t.blk_m}x{t.blk_n}x{t.blk_k}" + (f"b{band}" if band else "")
 
 
 def parse_tile(s: str) -> TileShape:
-    return TileShape(*(int(v) for v in s.split("x")))
+    """Inverse of :func:`tile_label`."""
+    dims, _, band = s.partition("b")
+    return kernel_tile(*(int(v) for v in dims.split("x")), int(band) if band else 0)
 
 
 @dataclass(frozen=True)

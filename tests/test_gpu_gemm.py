@@ -44,7 +44,26 @@ def _run(a, b, policy, tile, g=None, in_dtype=torch.bfloat16, out_dtype=torch.fl
     return c, plan
 
 
-POLICIES = None
+def _assert_trace(plan, m, n, k, tile, policy, band=0):
+    """Device trace == the oracle's build_schedule item for item (tile, kb, ke, write mode,
+    phase), and every item's C tile == locate_iter (band 0, the reference's order) or the
+    oracle's enumerated banded order."""
+    sk = _sk()
+    ref = osched.build_schedule(m, n, k, tile[0], tile[1], tile[2], plan.g, policy.kind.value,
+                                policy.sk_batches, policy.sk_first)
+    dev = plan.trace_items()
+    assert [[row[:5] for row in wg] for wg in dev] == ref, policy.label
+    mt, nt = -(-m // tile[0]), -(-n // tile[1])
+    want = osched.trace_coords(ref, mt, nt, band)
+    assert [[tuple(row[6:8]) for row in wg] for wg in dev] == want, (policy.label, band)
+    if band == 0:
+        grid = sk.grid_info(sk.ProblemSize(m, n, k), sk.TileShape(*tile[:3]))
+        for wg in dev:
+            for row in wg:
+                loc = sk.locate_iter(row[0] * grid.iters_per_tile + row[1], grid)
+                assert (loc.tile_m, loc.tile_n) == tuple(row[6:8])
+
+
 
 
 def _policies():
@@ -117,10 +136,7 @@ def test_device_trace_matches_closed_form_and_oracle():
     a, b = _int_case(1024, 1024, 1024, seed=1)
     for pol in _policies():
         _, plan = _run(a, b, pol, tile, trace_cap=64)
-        dev = plan.trace_items()
-        want = osched.build_schedule(size.m, size.n, size.k, 128, 128, 64, 148, pol.kind.value, pol.sk_batches, pol.sk_first)
-        got = [[(t, kb, ke, wm, ph) for (t, kb, ke, wm, ph, _role) in wg] for wg in dev]
-        assert got == want, pol.label
+        _assert_trace(plan, size.m, size.n, size.k, (128, 128, 64), pol)
 
 
 def test_cta_pair_trace_matches_oracle():
@@ -132,9 +148,7 @@ def test_cta_pair_trace_matches_oracle():
         got, plan = _run(a, b, pol, sk.TileShape(256, 256, 64), trace_cap=64)
         assert plan.g == 74
         assert np.array_equal(got.double().cpu().numpy(), want), pol.label
-        dev = [[row[:5] for row in wg] for wg in plan.trace_items()]
-        ref = osched.build_schedule(size.m, size.n, size.k, 256, 256, 64, 74, pol.kind.value, pol.sk_batches, pol.sk_first)
-        assert dev == ref, pol.label
+        _assert_trace(plan, size.m, size.n, size.k, (256, 256, 64), pol)
 
 
 def test_fp16_and_output_dtypes():
@@ -282,33 +296,27 @@ def test_fuzz_bitwise_and_trace(case):
     ref = osched.build_schedule(m, n, k, tile[0], tile[1], tile[2], g, policy.kind.value, policy.sk_batches,
                                 policy.sk_first)
     if max(len(w) for w in ref) <= 512:
-        dev = [[row[:5] for row in wg] for wg in plan.trace_items()]
-        assert dev == ref
+        _assert_trace(plan, m, n, k, tile, policy)
 
 
-@pytest.mark.parametrize("raster", [-1, 3, 8, 16])
+@pytest.mark.parametrize("band", [0, 3, 8, 16])
 @pytest.mark.parametrize("m,n,k,tile", [
     (2304, 3000, 1000, (256, 256, 64)),   # 9 x 12 = 108 pair tiles on 74 pairs: 1.5 waves
     (1500, 2600, 704, (128, 64, 64)),     # 12 x 41 = 492 tiles: >= 3 waves of 148
-    (4000, 4104, 520, (128, 128, 128)),   # 32 x 33 = 1056 tiles: 7 waves (auto -> banded)
+    (4000, 4104, 520, (128, 128, 128)),   # 32 x 33 = 1056 tiles: 7 waves
     (700, 9000, 304, (256, 128, 32)),     # 3 x 71 tile rows fewer than the band
 ])
-def test_banded_tile_order_bitwise_every_policy(raster, m, n, k, tile):
-    """The banded index -> C-tile map (skpp_set_raster) is a bijection: every policy stays
-    bit-exact against the oracle, and the device trace is still the reference schedule."""
+def test_banded_tile_order_bitwise_every_policy(band, m, n, k, tile):
+    """The banded tile order (KernelTile band_rows, skpp_tile_t.tile_order) is a bijection:
+    every policy stays bit-exact against the oracle, the device trace is still the reference
+    schedule, and each item's C tile is the oracle's enumerated banded order (band 0: the
+    reference's locate_iter)."""
     sk = _sk()
-    from paper_2408_11417_b200 import _lib
-
     a, b = _int_case(m, n, k, seed=m ^ n ^ k)
     want = ogemm.reference_gemm(a, b)
-    _lib.lib.skpp_set_raster(raster)
-    try:
-        for pol in (sk.Policy.data_parallel(), sk.Policy.hybrid(1), sk.Policy.hybrid(2, sk_first=False),
-                    sk.Policy.all_stream_k()):
-            got, plan = _run(a, b, pol, sk.TileShape(*tile), trace_cap=64)
-            assert np.array_equal(got.double().cpu().numpy(), want), (raster, pol.label)
-            ref = osched.build_schedule(m, n, k, tile[0], tile[1], tile[2], plan.g, pol.kind.value,
-                                        pol.sk_batches, pol.sk_first)
-            assert [[row[:5] for row in wg] for wg in plan.trace_items()] == ref
-    finally:
-        _lib.lib.skpp_set_raster(-1)
+    t = sk.kernel_tile(*tile, band)
+    for pol in (sk.Policy.data_parallel(), sk.Policy.hybrid(1), sk.Policy.hybrid(2, sk_first=False),
+                sk.Policy.all_stream_k()):
+        got, plan = _run(a, b, pol, t, trace_cap=64)
+        assert np.array_equal(got.double().cpu().numpy(), want), (band, pol.label)
+        _assert_trace(plan, m, n, k, tile, pol, band)

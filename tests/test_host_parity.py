@@ -257,6 +257,44 @@ def test_fixup_roles_and_ownership_invariants():
             assert xs == list(range(xs[0], xs[0] + len(xs)))
 
 
+def test_tile_order_closed_form_matches_oracle_enumeration():
+    """skpp_sched.h tile_coords (the map the kernel and its trace use) == the oracle's
+    enumerated order: band 0 is locate_iter (scheduler.py:155-165) and the host item rows carry
+    it; band G > 0 is a bijection onto the m_tiles x n_tiles grid."""
+    from paper_2408_11417_b200 import scheduler as ps
+
+    rng = np.random.default_rng(5)
+    for i in range(120):
+        m, n = int(rng.integers(1, 5000)), int(rng.integers(1, 5000))
+        bm, bn = int(rng.choice([128, 256])), int(rng.choice([64, 128, 256]))
+        band = int(rng.choice([0, 1, 2, 3, 8, 16, 64]))
+        sc = ps.closed_form(sk.ProblemSize(m, n, 64), sk.TileShape(bm, bn, 64), 148, CANON[i % 7])
+        mt, nt = int(sc.m_tiles), int(sc.n_tiles)
+        want = osc.banded_order(mt, nt, band)
+        got = [ps.tile_coords(sc, band, t) for t in range(mt * nt)]
+        assert got == want, (m, n, bm, bn, band)
+        assert sorted(got) == [(a, b) for a in range(mt) for b in range(nt)]
+        if band == 0:
+            items, _ = ps.schedule_arrays(sc)
+            grid = sk.grid_info(sk.ProblemSize(m, n, 64), sk.TileShape(bm, bn, 64))
+            for row in items[:50]:
+                loc = sk.locate_iter(int(row[0]) * grid.iters_per_tile + int(row[1]), grid)
+                assert (loc.tile_m, loc.tile_n) == (int(row[6]), int(row[7]))
+
+
+def test_kernel_tile_labels_round_trip():
+    from paper_2408_11417_b200 import tiles
+
+    for lab in ("128x128x64", "256x256x128b16", "128x64x128b8"):
+        t = tiles.parse_tile(lab)
+        assert tiles.tile_label(t) == lab
+        assert sk.tile_order(t) == (int(lab.split("b")[1]) if "b" in lab else 0)
+    assert type(tiles.parse_tile("128x128x64")) is sk.TileShape  # order 0 is the reference's TileShape
+    assert sk.kernel_tile(256, 256, 128, 16) != sk.TileShape(256, 256, 128)
+    with pytest.raises(ValueError):
+        sk.KernelTile(256, 256, 128, 0)
+
+
 def test_coverage_audit_matches_reference():
     for rec in GOLD["coverage"]:
         mt, nt, ipt, tt, ti = rec["grid"]

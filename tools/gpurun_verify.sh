@@ -15,6 +15,6 @@ timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/p
 for f in $O/memcheck_skinny.txt $O/racecheck_pair_skinny.txt; do tail -n 2 $f; done
 # banded tile order (RASTER instantiation; auto on >= 4 waves): memcheck + racecheck + synccheck
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_gemm.py -m gpu -q -k banded -p no:cacheprovider > $O/memcheck_banded.txt 2>&1; echo memcheck banded rc=$?
-timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/profile_gemm.py --m 4000 --n 4104 --k 520 --policy hybrid1 --tile 128x128x128 --iters 1 > $O/racecheck_banded.txt 2>&1; echo racecheck banded rc=$?
-timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/profile_gemm.py --m 4000 --n 4104 --k 520 --policy hybrid1 --tile 128x128x128 --iters 1 > $O/synccheck_banded.txt 2>&1; echo synccheck banded rc=$?
+timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/profile_gemm.py --m 4000 --n 4104 --k 520 --policy hybrid1 --tile 128x128x128b16 --iters 1 > $O/racecheck_banded.txt 2>&1; echo racecheck banded rc=$?
+timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/profile_gemm.py --m 4000 --n 4104 --k 520 --policy hybrid1 --tile 128x128x128b16 --iters 1 > $O/synccheck_banded.txt 2>&1; echo synccheck banded rc=$?
 for f in $O/memcheck_banded.txt $O/racecheck_banded.txt $O/synccheck_banded.txt; do tail -n 2 $f; done

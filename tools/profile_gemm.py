@@ -48,13 +48,11 @@ def main() -> None:
 
     if os.environ.get("SKPP_L2_HINTS"):
         _lib.lib.skpp_set_l2_hints(int(os.environ["SKPP_L2_HINTS"]))
-    if os.environ.get("SKPP_RASTER"):
-        _lib.lib.skpp_set_raster(int(os.environ["SKPP_RASTER"]))
 
     _lib.lib.skpp_set_b3d(args.b3d)
     dt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
     od = {"fp32": torch.float32, "bf16": torch.bfloat16, "fp16": torch.float16}[args.out]
-    tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
+    tile = sk.tiles.parse_tile(args.tile)  # "MxNxK" or "MxNxKbG" (banded tile order)
     a = torch.randn(args.m, args.k, device="cuda").to(dt)
     b = torch.randn(args.k, args.n, device="cuda").to(dt)
     c = torch.empty(args.m, args.n, device="cuda", dtype=od)
