@@ -32,6 +32,14 @@ from .types import Policy, ProblemSize, TileShape, kernel_tile, tile_order
 
 Config = tuple  # (TileShape, Policy)
 
+BANK_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "banks", "b200")
+
+
+def default_bank_dir() -> str:
+    """The tile bank shipped with the package: per-tile SKPS banks + manifest built from the
+    B200 sweep (``python -m paper_2408_11417_b200.sweep``), used by the bench and the CLI."""
+    return BANK_DIR
+
 
 def tile_label(t: TileShape) -> str:
     """``MxNxK`` for the reference's tile order, ``MxNxKbG`` for G-row bands (KernelTile)."""
@@ -315,6 +323,6 @@ def joint_records_from_csvs(paths_by_tile: list[tuple[TileShape, str]]) -> list[
 
 
 __all__ = [
-    "JointRecord", "Selector", "TileBank", "build_tile_bank", "evaluate_selection", "joint_records_from_csvs",
+    "BANK_DIR", "JointRecord", "Selector", "TileBank", "build_tile_bank", "default_bank_dir", "evaluate_selection", "joint_records_from_csvs",
     "joint_winner", "parse_tile", "snap_corners", "snap_pow2", "tile_label", "CostEstimate", "TuneRecord", "rank_costs",
 ]

@@ -185,7 +185,7 @@ def test_device_schedule_trace_kernel_matches_host():
         sc = scheduler.closed_form(size, tile, g, pol)
         items, offsets = scheduler.schedule_arrays(sc)
         cap = int(max(offsets[x + 1] - offsets[x] for x in range(g)))
-        trace = torch.full((g, cap, 6), -1, dtype=torch.int64, device="cuda")
+        trace = torch.full((g, cap, _lib.TRACE_FIELDS), -1, dtype=torch.int64, device="cuda")
         counts = torch.zeros(g, dtype=torch.int64, device="cuda")
         _lib.check(_lib.lib.skpp_schedule_trace_device(
             _lib.Problem(size.m, size.n, size.k), _lib.Tile(tile.blk_m, tile.blk_n, tile.blk_k),
