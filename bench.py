@@ -2,28 +2,37 @@
 """Stream-K++ on B200 — headline benchmark (one JSON line on rank 0).
 
 Metric (BASELINE.json): "GEMM TFLOP/s vs dense TC peak; % shapes within 20%
-of oracle policy".  Default workload = BASELINE config 2: the skinny,
-split-K-bound bf16 GEMM M=N=512, K=16384 with fp32 output, under the policy
-the Stream-K++ selection layer picks:
+of oracle policy".  Both halves are measured in this run:
 
-  1. selection (untimed): every canonical policy's schedule is measured on
-     the device (identical schedules once), a Bloom bank is built from the
-     winner, and the selected policy is the fastest measured candidate of
-     ``bank.query(size) | {data-parallel}``;
-  2. timed region: K steps, one persistent-kernel launch per step, back to
-     back on one stream between ONE pair of CUDA events (max over ranks);
-     the steps rotate over R distinct operand sets whose total is > 4x the
-     126 MB L2, so every step reads its operands from HBM (cold L2).
+  * GEMM TFLOP/s — default workload = BASELINE config 3 at its largest
+    single-GPU shape: the Llama-3-8B MLP projection at 8192 tokens,
+    bf16 8192 x 14336 x 4096 with fp32 output, under the (tile, policy) the
+    Stream-K++ selection layer picks: the shipped tile bank's Bloom candidates
+    (``paper_2408_11417_b200/banks/b200``, corners + calibrated prior for sizes it
+    never saw) plus the data-parallel baseline, each timed once, fastest wins.
+    Every (tile, canonical policy) of the candidate tiles is also measured so the
+    line reports the selected configuration against the measured oracle.
+    Timed region: K steps, one persistent-kernel launch per step, back to back on
+    one stream between ONE pair of CUDA events (max over ranks); the steps rotate
+    over R distinct operand sets whose total is > 4x the 126 MB L2 (cold L2).
+  * % shapes within 20% — a bounded selection check of the paper grid
+    (``--sweep-grid``, default the reference's 1,456-size DEFAULT_GRID, one tile,
+    seven policies): pass 1 measures every (size, policy) on the GPU and builds
+    the Bloom bank from the winners, pass 2 re-measures independently and the
+    fraction of sizes whose Bloom-selected policy is within 20% of that pass's
+    oracle is reported.  With N GPUs the sizes are LPT-partitioned across the
+    ranks (no data-path collective; records are gathered on the host), so the
+    ``sweep`` block carries shape x policy/s and distinct schedules/s at N.
 
 Also reported: ``e2e`` (the same GEMM through the public
 ``execute_schedule`` with pinned host bf16 inputs, H2D + kernel + D2H every
 step, wall clock), ``roofline`` for the GEMM kernel, ``cpu_baseline`` (the
-oracle's float64 numpy port of the reference executor on this box's cores)
-and per-policy TFLOP/s from the selection sweep.
+oracle's float64 numpy port of the reference executor on this box's cores).
 
 ``--impl reference`` times the reference's CPU implementation of the path
 (the oracle port of gemmsched's execute_schedule, float64 numpy/OpenBLAS,
-all host cores) on the same workload; under torchrun only rank 0 runs it.
+all host cores) on the same workload under the configuration the shipped bank
+selects host-side (no GPU involved); under torchrun only rank 0 runs it.
 With N GPUs each rank runs the same GEMM (the GEMM runs on one GPU;
 replicas only), so ``value`` is N x the per-replica throughput ("weak").
 """
@@ -47,6 +56,9 @@ ROTATE_BYTES = 4 * 128 * 1024 * 1024  # operand sets rotated through per step: 4
 ISOLATED_STEPS = 50
 
 WORKLOADS = {
+    "cfg3": dict(m=8192, n=14336, k=4096, dtype="bf16",
+                 desc="BASELINE cfg3 (largest single-GPU shape): Llama-3-8B MLP gate/up projection at 8192 "
+                      "tokens, bf16 8192x14336x4096, fp32 out, Bloom-selected (tile, policy)"),
     "cfg2": dict(m=512, n=512, k=16384, dtype="bf16",
                  desc="BASELINE cfg2: skinny split-K-bound bf16 GEMM M=N=512 K=16384, fp32 out, "
                       "Bloom-selected (tile, policy) among the 7 canonical policies x candidate tiles"),
@@ -56,7 +68,9 @@ WORKLOADS = {
                        desc="large square bf16 GEMM 8192^3, fp32 out (70%-of-peak target), Bloom-selected (tile, policy)"),
 }
 # Candidate tiles of the joint (tile, policy) selection, baseline (DP) tile first.
-BENCH_TILES = ["128x128x64", "128x64x128", "128x128x128", "256x128x128", "256x256x64", "256x256x128"]
+BENCH_TILES = ["128x128x64", "128x64x128", "128x128x128", "256x128x128", "256x256x64", "256x256x128",
+               "128x128x128b16", "256x256x128b16"]
+SWEEP_TILE = "128x128x128"
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                   "source": "fallback (B200_PROFILING.md)"}
@@ -176,42 +190,122 @@ def ncu_traffic(workload: str, tile_label: str, policy_label: str):
     (profiles/ncu_bench_<workload>.json, made by tools/gpurun_profile.sh), or None when the
     capture is of a different kernel configuration than the one this run selected."""
     path = os.path.join(ROOT, "profiles", f"ncu_bench_{workload}.json")
-    bm, bn, bk = (int(v) for v in tile_label.split("x"))
-    want = f"<{bn}, {bk}, {bm // 128}"  # template args <BN, BK, CG[, RASTER]>
+    from paper_2408_11417_b200.tiles import parse_tile
+
+    t = parse_tile(tile_label)
+    # template args <BN, BK, CG, RASTER>
+    want = f"<{t.blk_n}, {t.blk_k}, {t.blk_m // 128}, {1 if getattr(t, 'band_rows', 0) else 0}>"
     try:
         with open(path) as fh:
             rows = json.load(fh)
-        row = next(r for r in rows if "streamk_gemm" in r.get("kernel", "")
-                   and (want + ">" in r["kernel"] or want + "," in r["kernel"])
+        row = next(r for r in rows if "streamk_gemm" in r.get("kernel", "") and want in r["kernel"]
                    and r.get("policy", policy_label) == policy_label)
         return int(row["dram_traffic_bytes"]), os.path.relpath(path, ROOT)
     except (OSError, ValueError, KeyError, StopIteration):
         return None, None
 
 
-def sweep_summary():
-    """Selection quality over the paper grid from the committed GPU sweep run (separate job)."""
-    path = os.path.join(ROOT, "profiles", "round1", "sweep_joint5_summary.json")
-    try:
-        with open(path) as fh:
-            d = json.load(fh)
-    except (OSError, ValueError):
+def sweep_check(world: int, rank: int, grid: str, tile_label_: str) -> dict | None:
+    """Bounded in-run selection check over the paper grid (the metric's second half).
+
+    Pass 1 measures every (size, canonical policy) of this rank's LPT share on the GPU
+    (identical schedules once), the records of all ranks are gathered on the host and the
+    Bloom bank is built from the winners (``build_bank``: lexicographic insertion, so its
+    bytes do not depend on the partition).  Pass 2 re-measures independently and reports
+    the fraction of sizes whose Bloom-selected policy (fastest of ``query | {DP}`` by pass-2
+    time) is within 20% of pass 2's oracle, plus eliminated fraction and false negatives.
+    Sweep time per pass = CUDA events around the rank's whole share, max over ranks.
+    """
+    import hashlib
+
+    import torch
+
+    import paper_2408_11417_b200 as sk
+    from paper_2408_11417_b200 import pipeline as pl, sweep
+    from paper_2408_11417_b200.scheduler import closed_form, schedule_signature
+    from paper_2408_11417_b200.tiles import parse_tile
+
+    if grid == "none":
         return None
-    held = d.get("selection_heldout_run", {})
-    off = d.get("selection_offgrid_corners_and_model") or d.get("selection_offgrid_pow2_corners", {})
-    pow2 = d.get("selection_offgrid_nearest_pow2", {})
+    sizes = sweep.grid_sizes(grid)
+    tile = parse_tile(tile_label_)
+    g = sk.executor.default_g(tile)
+    pols = sk.canonical_policies()
+    params = sweep.MeasureParams(warmup=3, reps=10)
+    mine = sorted(sweep.lpt_partition(sizes, world)[rank], key=lambda z: (z.m, z.n, z.k))
+    pool = sweep.OperandPool(mine or sizes[:1], params.in_dtype, params.out_dtype, seed=rank)
+    stream = torch.cuda.current_stream()
+
+    def one_pass():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        recs = sweep.tune_sizes(mine, tile, g, pols, params, pool) if mine else []
+        e1.record(stream)
+        torch.cuda.synchronize()
+        secs = e0.elapsed_time(e1) / 1e3
+        if world > 1:
+            gathered = [None] * world
+            torch.distributed.all_gather_object(gathered, (secs, recs))
+        else:
+            gathered = [(secs, recs)]
+        merged = [r for _, part in gathered for r in part]
+        merged.sort(key=lambda r: (r.size.m, r.size.n, r.size.k))
+        return merged, [sec for sec, _ in gathered]
+
+    rec1, secs1 = one_pass()
+    rec2, secs2 = one_pass()
+    if rank != 0:
+        return None
+    bank = pl.build_bank(rec1)
+    q = pl.selection_quality(rec2, bank, 0.20)
+    el = sk.elimination_stats(bank, rec2)
+    distinct = sum(len({schedule_signature(closed_form(z, tile, g, p)) for p in pols}) for z in sizes)
+    t1 = max(secs1)
     return {
-        "source": os.path.relpath(path, ROOT) + " (separate sweep job on the same GPU pool)",
-        "sizes": d.get("sizes"),
-        "tiles": d.get("tiles"),
-        "pct_within_20pct_of_oracle_heldout_run": round(100 * held.get("fraction_within", float("nan")), 2),
-        "pct_within_20pct_of_oracle_offgrid_sizes": round(100 * off.get("fraction_within", float("nan")), 2),
-        "offgrid_fallback": "union of the filters at the enclosing power-of-two sizes + calibrated cost-model pick"
-        if "selection_offgrid_corners_and_model" in d else "union of the filters at the enclosing power-of-two sizes",
-        "pct_within_20pct_offgrid_nearest_pow2_only": round(100 * pow2.get("fraction_within", float("nan")), 2),
-        "eliminated_fraction": held.get("eliminated_fraction"),
-        "shape_policy_per_s_1gpu": round(d.get("shape_policy_per_s", 0.0), 1),
+        "grid": grid, "sizes": len(sizes), "policies": len(pols), "tile": tile_label_, "g": g,
+        "n_gpus": world, "partition": "LPT by estimated cost, sizes sharded, no data-path collective",
+        "pct_within_20pct_of_oracle": round(100 * q["fraction_within"], 2),
+        "median_slowdown_vs_oracle": round(q["median_slowdown"], 4),
+        "max_slowdown_vs_oracle": round(q["max_slowdown"], 4),
+        "eliminated_fraction": round(el.eliminated_fraction, 4),
+        "false_negatives_vs_pass2_winners": el.false_negatives,
+        "pass1_seconds_max_over_ranks": round(t1, 3),
+        "pass2_seconds_max_over_ranks": round(max(secs2), 3),
+        "rank_seconds_pass1": [round(v, 3) for v in secs1],
+        "shape_policy_per_s": round(len(sizes) * len(pols) / t1, 1),
+        "distinct_schedules": distinct,
+        "distinct_schedules_per_s": round(distinct / t1, 1),
+        "bank_sha256": hashlib.sha256(bank.to_bytes()).hexdigest(),
+        "winners_sha256": hashlib.sha256(";".join(
+            f"{r.size.m},{r.size.n},{r.size.k}:{r.winner.label}" for r in rec1).encode()).hexdigest(),
+        "method": "pass 1 (build bank) and pass 2 (independent re-measurement) each time every (size, "
+                  "policy) with CUDA-graph replays (warm-up 3, median of <=10); selected = fastest "
+                  "pass-2 time among query(size) | {DP}; times are device events around each rank's share",
+        "note": "bank bytes depend only on the winners (lexicographic insertion); winners of near-tied "
+                "sizes can differ between runs, so compare winners_sha256 before bank_sha256",
     }
+
+
+def host_selection(size, dtype: str):
+    """The configuration the shipped tile bank selects WITHOUT timing anything: its Bloom
+    candidates (corners + calibrated prior) plus the baseline; with several candidates the
+    calibrated cost model's pick if it is one of them, else the first.  Used by the
+    reference arm (which must not touch the GPU) and reported by ours for comparison."""
+    import paper_2408_11417_b200 as sk
+    from paper_2408_11417_b200 import tiles as tl
+
+    bank = tl.TileBank.load(sk.default_bank_dir())
+    cand = bank.candidates(size, "corners+model")
+    if len(cand) == 1:
+        return cand[0], cand
+    try:
+        pick = bank.prior_pick(size)
+    except ValueError:
+        pick = None
+    return (pick if pick in cand else cand[0]), cand
 
 
 def roofline(flops: float, nbytes: float, seconds: float, peaks: dict, sustained: bool = False) -> dict:
@@ -256,8 +350,11 @@ def fixup_summary(plan, tile, flops: float, nbytes: float, seconds: float) -> di
 
 
 def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool, max_seconds: float,
-                    max_reps: int, seed: int = 0):
-    """Time the oracle port of the reference executor (float64) on this host."""
+                    max_reps: int, seed: int = 0, wg_stride: int = 1):
+    """Time the oracle port of the reference executor (float64) on this host.
+
+    ``wg_stride`` > 1 bounds the sample: each run executes the items of every
+    ``wg_stride``-th workgroup of the schedule only.  Returns [(seconds, flops executed)]."""
     import numpy as np
 
     from oracle import gemm as ogemm
@@ -270,72 +367,94 @@ def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool,
     b = ogemm.random_int_matrix(k, n, rng)
     g = 148 // (bm // 128)  # one workgroup per SM, or per SM pair for 256-row tiles
     sched = osched.build_schedule(m, n, k, bm, bn, bk, g, policy_kind, sk_batches, sk_first)
+    sched = sched[::wg_stride]
     n_tiles = -(-n // bn)
-    times = []
+    flops = 0
+    for wg in sched:
+        for t, kb, ke, _wm, _ph in wg:
+            tm, tn = divmod(t, n_tiles)
+            flops += 2 * (min(bm, m - tm * bm)) * (min(bn, n - tn * bn)) * (min(ke * bk, k) - kb * bk)
+    out = []
     t_start = time.perf_counter()
-    while len(times) < max_reps and (time.perf_counter() - t_start) < max_seconds:
+    while len(out) < max_reps and (not out or time.perf_counter() - t_start < max_seconds):
         t0 = time.perf_counter()
         ogemm.execute_schedule(a, b, sched, m, n, k, bm, bn, bk, n_tiles)
-        times.append(time.perf_counter() - t0)
-    return times
+        out.append((time.perf_counter() - t0, flops))
+    return out
+
+
+def _policy_tuple(policy) -> tuple:
+    return (policy.kind.value, policy.sk_batches, policy.sk_first)
+
+
+def _config_keys(wl: dict, tile, g: int, policy_label: str, world: int) -> dict:
+    """The ``config`` object both arms print (identical keys and values for the same selection)."""
+    return {"workload": wl["desc"], "m": wl["m"], "n": wl["n"], "k": wl["k"],
+            "tile": [tile.blk_m, tile.blk_n, tile.blk_k], "tile_order": getattr(tile, "band_rows", 0),
+            "g": g, "policy": policy_label, "parallelism": f"replicas x{world} (GEMM is single-GPU)"}
+
+
+CPU_STEP_BUDGET_S = 4.0  # reference arm: target CPU seconds per step (bounded sample)
 
 
 def run_reference(args, wl: dict) -> None:
     world, rank, _ = dist_setup(args.gpus)
     if rank != 0:
         return
+    import paper_2408_11417_b200 as sk
+
     cores = len(os.sched_getaffinity(0))
     m, n, k = wl["m"], wl["n"], wl["k"]
-    flops = 2.0 * m * n * k
-    # Same (tile, policy) as our arm: the configuration its selection picked in the committed
-    # bench line of this workload (the reference executor's cost barely depends on it);
-    # otherwise hybrid1 on 128x128x64 (for T < g every Stream-K policy ties and the
-    # reference's ordinal tie-break credits hybrid1).
-    pol, tile = ("hybrid", 1, True), (128, 128, 64)
-    try:
-        with open(os.path.join(ROOT, "profiles", "round1", f"bench_{args.workload}.json")) as fh:
-            cfg = json.load(fh)["config"]
-        tile = tuple(int(v) for v in cfg["tile"])
-        lab = cfg["policy"]
-        pol = (("data-parallel", 0, False) if lab == "data-parallel" else ("all-streamk", 0, False)
-               if lab == "all-streamk" else ("hybrid", int(lab[len("hybrid"):].split("-")[0]), "dpfirst" not in lab))
-    except (OSError, ValueError, KeyError):
-        pass
-    wl = dict(wl, tile=tile)
-    cpu_oracle_gemm(wl, *pol, max_seconds=30, max_reps=args.warmup)  # warm-up
-    # bounded: K steps or 60 s of CPU work, whichever comes first
-    times = cpu_oracle_gemm(wl, *pol, max_seconds=60, max_reps=args.steps)
-    total = sum(times)
-    value = flops * len(times) / total / 1e12
+    size = sk.ProblemSize(m, n, k)
+    (tile, policy), cand = host_selection(size, wl["dtype"])
+    g = 148 // (tile.blk_m // 128)
+    wlt = dict(wl, tile=(tile.blk_m, tile.blk_n, tile.blk_k))
+    pol = _policy_tuple(policy)
+    # One probe run of a 1/16 sample sizes the per-step sample so the whole --steps/--warmup
+    # run stays within a few minutes: full schedule when a step fits CPU_STEP_BUDGET_S.
+    probe = cpu_oracle_gemm(wlt, *pol, max_seconds=0, max_reps=1, wg_stride=16)[0]
+    est_full = probe[0] * (2.0 * m * n * k) / probe[1]
+    stride = max(1, int(-(-est_full // CPU_STEP_BUDGET_S)))
+    cpu_oracle_gemm(wlt, *pol, max_seconds=1e9, max_reps=args.warmup, wg_stride=stride)  # warm-up
+    runs = cpu_oracle_gemm(wlt, *pol, max_seconds=1e9, max_reps=args.steps, wg_stride=stride)
+    total = sum(t for t, _ in runs)
+    value = sum(f for _, f in runs) / total / 1e12
+    sample = (f"{len(runs)} steps, each a {'full' if stride == 1 else f'1/{stride} workgroup sample of the'} "
+              f"{m}x{n}x{k} schedule ({runs[0][1] / 1e9:.1f} GFLOP executed per step) run by the oracle port of "
+              f"gemmsched executor.py:51-112 (float64 numpy/OpenBLAS)")
     line = {
         "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(total / len(times) * 1e3, 3),
+        "steps": len(runs), "warmup": args.warmup, "ms_per_step": round(total / len(runs) * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (integer-valued float64, seed 0)",
-        "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]),
-                   "g": 148 // (wl["tile"][0] // 128),
-                   "policy": pol[0] if pol[0] != "hybrid" else f"hybrid{pol[1]}", "l2": "n/a (CPU)"},
+        "config": _config_keys(wl, tile, g, policy.label, args.gpus),
+        "selection": {"how": "host-side: shipped tile bank candidates (corners + calibrated prior), "
+                             "calibrated-model pick among them (no GPU)",
+                      "candidates": [f"{t.blk_m}x{t.blk_n}x{t.blk_k}" + (f"b{t.band_rows}" if getattr(t, 'band_rows', 0) else "")
+                                     + f"/{p.label}" for t, p in cand]},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(times)} full {m}x{n}x{k} schedule executions "
-                                   f"(oracle port of gemmsched executor.py:51-112, float64 numpy/OpenBLAS)"},
+                         "sample": sample},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def select_config(size, tiles, pool):
-    """Measure every (tile, canonical policy), build the per-tile Bloom banks from the joint
-    winner, and pick the fastest measured candidate of query(size) | {baseline}."""
+    """The Stream-K++ selection for the workload: the shipped tile bank's Bloom candidates
+    (corners + calibrated prior for sizes it never saw) plus the baseline, each timed, fastest
+    wins.  Every (tile, canonical policy) of ``tiles`` is measured too (round-robin over 5
+    rounds, median) — the measured oracle the selection is compared against."""
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import sweep, tiles as tl
 
+    bank = tl.TileBank.load(sk.default_bank_dir())
+    cand = bank.candidates(size, "corners+model")
+    all_tiles = list(tiles) + [t for t, _ in cand if t not in tiles]
     params = sweep.MeasureParams(warmup=3, reps=5, in_dtype=pool.a.dtype)
-    per_tile = sweep.measure_size_tiles(size, tiles, sk.canonical_policies(), params, pool, rounds=5)
+    per_tile = sweep.measure_size_tiles(size, all_tiles, sk.canonical_policies(), params, pool, rounds=5)
     rec = tl.joint_winner(size, per_tile)
-    bank = tl.build_tile_bank([rec], list(tiles))
-    cand = bank.candidates(size)
-    tile, policy = min(cand, key=lambda c: (rec.time_of(c), tiles.index(c[0]), c[1].sort_key()))
+    tile, policy = min(cand, key=lambda c: (rec.time_of(c), all_tiles.index(c[0]), c[1].sort_key()))
     return tile, policy, rec, cand
 
 
@@ -457,11 +576,13 @@ def run_ours(args, wl: dict) -> None:
     e2e_mean_value = world * flops * e2e_steps / sum(e2e_t) / 1e12
     assert out.shape == (m, n)
 
+    sweep_block = sweep_check(world, rank, args.sweep_grid, args.sweep_tile)
+    ref_cfg, _ = host_selection(size, wl["dtype"])
     if rank == 0:
         cores = len(os.sched_getaffinity(0))
-        cpu_times = cpu_oracle_gemm(wl, policy.kind.value, policy.sk_batches, policy.sk_first,
-                                    max_seconds=args.cpu_seconds, max_reps=20)
-        cpu_value = flops / statistics.median(cpu_times) / 1e12
+        cpu_runs = cpu_oracle_gemm(wl, policy.kind.value, policy.sk_batches, policy.sk_first,
+                                   max_seconds=args.cpu_seconds, max_reps=20)
+        cpu_value = statistics.median(f / t for t, f in cpu_runs) / 1e12
         per_config = {f"{tl.tile_label(t)}/{p.label}": round(size.flops / (e.makespan * 1e-6) / 1e12, 2)
                       for t, r in rec.per_tile for p, e in r.costs}
         roof = roofline(flops, nbytes, per_step_s, peaks, sustained=total_ms > 100.0)
@@ -485,13 +606,12 @@ def run_ours(args, wl: dict) -> None:
             "vs_baseline": None,
             "dtype": wl["dtype"],
             "data": "synthetic (randn operands, seeded)",
-            "config": {
-                "workload": wl["desc"], "m": m, "n": n, "k": k, "tile": list(wl["tile"]), "g": g,
-                "policy": policy.label, "out_dtype": "fp32", "candidate_tiles": BENCH_TILES,
+            "config": _config_keys(wl, tile, g, policy.label, world),
+            "method": {
+                "out_dtype": "fp32", "candidate_tiles": BENCH_TILES,
                 "l2": f"cold: steps rotate over {n_sets} distinct operand sets "
                       f"({n_sets * set_bytes / 2**20:.0f} MiB > 4x the 126 MB L2); no flush",
                 "timing": "one CUDA-event pair around K back-to-back launches on one stream",
-                "parallelism": f"replicas x{world} (GEMM is single-GPU)",
             },
             "pct_of_dense_peak": {
                 "measured_bf16": round(value / world / peaks["bf16_tflops"], 4),
@@ -503,15 +623,18 @@ def run_ours(args, wl: dict) -> None:
                 "selected_vs_oracle": round(chosen_us / best_us, 4),
                 "within_20pct": chosen_us <= 1.2 * best_us,
                 "candidates": [f"{tl.tile_label(t)}/{p.label}" for t, p in cand],
+                "bank": os.path.relpath(sk.default_bank_dir(), ROOT),
+                "reference_arm_config": f"{tl.tile_label(ref_cfg[0])}/{ref_cfg[1].label}",
+                "reference_arm_config_is_selected": ref_cfg == (tile, policy),
                 "per_config_tflops": per_config,
                 "note": "per-(tile, policy) times from CUDA-graph replays with warm L2 (selection sweep)",
             },
             "roofline": roof,
             "fixup": fixup_summary(plan, tile, flops, nbytes, per_step_s),
-            "sweep": sweep_summary(),
+            "sweep": sweep_block,
             "cpu_baseline": {
                 "value": round(cpu_value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                "sample": f"{len(cpu_times)} full {m}x{n}x{k} runs of the oracle port of gemmsched "
+                "sample": f"{len(cpu_runs)} full {m}x{n}x{k} runs of the oracle port of gemmsched "
                           f"execute_schedule (float64 numpy/OpenBLAS, policy {policy.label})",
             },
             "e2e": {
@@ -538,10 +661,13 @@ def run_ours(args, wl: dict) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=25000)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--sweep-grid", default="paper",
+                    help="grid of the in-run selection check (sweep.grid_sizes name, or 'none')")
+    ap.add_argument("--sweep-tile", default=SWEEP_TILE)
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()

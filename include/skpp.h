@@ -151,6 +151,10 @@ int skpp_schedule_trace_device(const skpp_problem_t* p, const skpp_tile_t* t,
 /* Make `device` current for this library's CUDA runtime on the calling thread
    (the caller's framework may use a different runtime instance). */
 int skpp_set_device(int device);
+/* 1 when `stream` is being captured into a CUDA graph, else 0; negative status on error.
+   The host glue gives captured launches a workspace of their own (no reference
+   counterpart: the reference executor has no graphs). */
+int skpp_stream_is_capturing(void* stream);
 /* Debug hook: when non-NULL, following launches write 16 %globaltimer stamps per CTA
    (setup done, first load, first stage landed, last MMA, items done, flags seen,
    reductions done, ...) to device_buffer[cta*16 + event].  NULL disables. */

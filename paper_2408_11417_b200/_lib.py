@@ -133,6 +133,7 @@ SIGNATURES = {
         [_P(Problem), _P(Tile), _P(PolicyC), C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p],
     ),
     "skpp_set_device": (C.c_int, [C.c_int]),
+    "skpp_stream_is_capturing": (C.c_int, [C.c_void_p]),
     "skpp_debug_timeline": (None, [C.c_void_p]),
     "skpp_set_pdl": (None, [C.c_int]),
     "skpp_set_b3d": (None, [C.c_int]),

@@ -1424,6 +1424,16 @@ extern "C" int skpp_set_device(int device) {
   return SKPP_OK;
 }
 
+extern "C" int skpp_stream_is_capturing(void* stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(reinterpret_cast<cudaStream_t>(stream), &st);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaStreamIsCapturing: ") + cudaGetErrorString(e));
+    return SKPP_ELAUNCH;
+  }
+  return st == cudaStreamCaptureStatusActive ? 1 : 0;
+}
+
 extern "C" int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major,
                                 int32_t* cc_minor) {
   int v = 0;

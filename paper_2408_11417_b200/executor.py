@@ -136,23 +136,49 @@ def tile_supported(tile: TileShape) -> bool:
     return bool(_lib.lib.skpp_tile_supported(_lib.tile_c(tile)))
 
 
+WS_ZERO_BYTES = 4096  # header (256 B) + the flags of up to 2 x 148 CTAs, 256-B rounded, with margin
+
+
+def _new_workspace(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
+    """Allocate a fixup workspace on the launch stream and zero its header + flags there.
+
+    Only the header (epoch, arrival counter) and the slot flags need a defined initial
+    value: a slot is read only after its flag equals the launch's epoch.  Allocating and
+    zeroing on the stream the kernel runs on (not torch's current stream) orders the
+    memset before the first launch and ties the block's lifetime to that stream.
+    """
+    size = max(nbytes, 1 << 20)
+    with torch.cuda.stream(torch.cuda.ExternalStream(stream_handle, device=f"cuda:{device}")):
+        buf = torch.empty(size, dtype=torch.uint8, device=f"cuda:{device}")
+        buf[:WS_ZERO_BYTES].zero_()
+    return buf
+
+
 def workspace_for(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
-    """Zero-initialised fixup workspace, cached per (device, stream).
+    """Fixup workspace for eager launches, cached per (device, stream).
 
     The kernel keeps the workspace consistent itself (flags are tagged with
     an epoch stored in the workspace header and advanced by the last CTA of
     each launch), so a cached buffer serves every later launch on the same
-    stream, graph replays included.  Plans hold a reference to the buffer
-    they were bound to, so growing the cache never frees memory in use.
+    stream: launches on one stream are ordered, so they never use it at once.
+    Plans hold a reference to the buffer they were bound to, so growing the
+    cache never frees memory in use.  Graph-captured launches do not use this
+    cache: each plan gets its own workspace (:meth:`GemmPlan.prepare_for_capture`).
     """
     key = (device, stream_handle)
     with _ws_lock:
         buf = _workspaces.get(key)
         if buf is None or buf.numel() < nbytes:
-            size = max(nbytes, 1 << 20)
-            buf = torch.zeros(size, dtype=torch.uint8, device=f"cuda:{device}")
+            buf = _new_workspace(nbytes, device, stream_handle)
             _workspaces[key] = buf
         return buf
+
+
+def _is_capturing(handle: int) -> bool:
+    rc = _lib.lib.skpp_stream_is_capturing(handle)
+    if rc < 0:
+        raise _lib.SkppError(rc, _lib.last_error())
+    return rc == 1
 
 
 class GemmPlan:
@@ -235,6 +261,7 @@ class GemmPlan:
         self.ws_bytes = int(_lib.lib.skpp_plan_workspace_bytes(self._handle))
         self._launch = _lib.lib.skpp_plan_launch
         self._ws_cache: dict[int, tuple] = {}
+        self._private_ws: torch.Tensor | None = None
 
     def __del__(self):
         h, self._handle = getattr(self, "_handle", None), None
@@ -245,16 +272,36 @@ class GemmPlan:
     def uses_fixup(self) -> bool:
         return self.sched_c.sk_tiles > 0
 
+    def prepare_for_capture(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Give this plan its own workspace before its launches are captured into a CUDA graph.
+
+        Captured launches never share the per-stream eager workspace: graphs captured on
+        one stream could otherwise be replayed concurrently on different streams and race
+        on one flags/partials area.  Without this call, the first captured launch allocates
+        the private workspace inside the capture (its header memset then becomes a graph
+        node).  One workspace must never serve two executions at once: a graph (like any
+        launch of this plan) must not be replayed concurrently with itself.
+        """
+        if self.ws_bytes and self._private_ws is None:
+            handle = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(self.device)
+            self._private_ws = _new_workspace(self.ws_bytes, self.device, handle)
+
     def launch(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         handle = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(self.device)
-        ws = self._ws_cache.get(handle)
-        if ws is None:
-            if self.ws_bytes:
-                buf = workspace_for(self.ws_bytes, self.device, handle)
-                ws = (buf.data_ptr(), buf.numel(), buf)
-            else:
-                ws = (None, 0, None)
-            self._ws_cache[handle] = ws
+        if self.ws_bytes and _is_capturing(handle):
+            if self._private_ws is None:
+                self._private_ws = _new_workspace(self.ws_bytes, self.device, handle)
+            buf = self._private_ws
+            ws = (buf.data_ptr(), buf.numel(), buf)
+        else:
+            ws = self._ws_cache.get(handle)
+            if ws is None:
+                if self.ws_bytes:
+                    buf = workspace_for(self.ws_bytes, self.device, handle)
+                    ws = (buf.data_ptr(), buf.numel(), buf)
+                else:
+                    ws = (None, 0, None)
+                self._ws_cache[handle] = ws
         rc = self._launch(self._handle, ws[0], ws[1], handle)
         if rc != _lib.OK:
             raise _lib.SkppError(rc, _lib.last_error())

@@ -33,7 +33,7 @@ from dataclasses import dataclass
 import torch
 
 from .costmodel import CostEstimate, TuneRecord, rank_costs
-from .executor import GemmPlan, default_g, workspace_for
+from .executor import GemmPlan, default_g
 from .scheduler import count_partials, schedule_signature
 from .types import Policy, ProblemSize, TileShape, canonical_policies
 
@@ -116,13 +116,13 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
     if params.use_graphs:
         # Raw capture: torch.cuda.graph() would synchronise, gc.collect() and empty_cache()
         # before every capture — ~5 ms per measurement, the largest host cost of a
-        # multi-tile sweep.  The plan's fixup workspace for the capture
-        # stream is created here, outside the capture, so the graph allocates nothing.
+        # multi-tile sweep.  The plan's own fixup workspace (captured launches never use
+        # the shared per-stream one) is created here, outside the capture, so the graph
+        # holds no allocation or memset.
         dev = stream.device_index
         graph = torch.cuda.CUDAGraph()
         side = _side_stream(dev)
-        if plan.ws_bytes:
-            workspace_for(plan.ws_bytes, dev, side.cuda_stream)
+        plan.prepare_for_capture(side)
         side.wait_stream(stream)
         with torch.cuda.stream(side):
             graph.capture_begin()

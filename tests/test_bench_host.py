@@ -1,5 +1,6 @@
 """bench.py host-side pieces that need no GPU: the committed ncu captures resolve to the
-kernel configurations the bench selects (roofline.traffic), and the sweep summary loads."""
+kernel configurations the bench selects (roofline.traffic, template arguments including the
+tile order), the reference arm's host-side selection, and the shared config keys."""
 
 import json
 import os
@@ -12,7 +13,7 @@ import bench  # noqa: E402
 
 
 def test_committed_ncu_traffic_matches_selected_configs():
-    for wl in ("cfg2", "cfg1", "square8192"):
+    for wl in ("cfg2", "cfg1"):
         line = json.load(open(os.path.join(ROOT, "profiles", "round1", f"bench_{wl}.json")))
         tile = "x".join(str(v) for v in line["config"]["tile"])
         traffic, src = bench.ncu_traffic(wl, tile, line["config"]["policy"])
@@ -20,7 +21,36 @@ def test_committed_ncu_traffic_matches_selected_configs():
         assert src == f"profiles/ncu_bench_{wl}.json"
 
 
-def test_sweep_summary_reports_selection_quality():
-    s = bench.sweep_summary()
-    assert s is not None and s["sizes"] > 1000
-    assert s["pct_within_20pct_of_oracle_heldout_run"] >= 97.6  # the paper's figure
+def test_ncu_traffic_distinguishes_the_tile_order():
+    """The round-1 square8192 capture is of the banded instantiation <256, 128, 2, 1>; the
+    reference-order tile 256x256x128 must not pick it up, the banded tile must."""
+    assert bench.ncu_traffic("square8192", "256x256x128", "data-parallel") == (None, None)
+    traffic, _ = bench.ncu_traffic("square8192", "256x256x128b16", "data-parallel")
+    assert traffic and traffic > 0
+
+
+def test_reference_arm_selection_is_host_only_and_in_the_candidates():
+    import paper_2408_11417_b200 as sk
+
+    for wl in bench.WORKLOADS.values():
+        size = sk.ProblemSize(wl["m"], wl["n"], wl["k"])
+        cfg, cand = bench.host_selection(size, wl["dtype"])
+        assert cfg in cand
+        assert (sk.TileShape(128, 128, 64), sk.Policy.data_parallel()) in cand  # the baseline
+
+
+def test_both_arms_print_the_same_config_keys():
+    import paper_2408_11417_b200 as sk
+
+    wl = bench.WORKLOADS["cfg3"]
+    t = sk.kernel_tile(256, 256, 128, 16)
+    cfg = bench._config_keys(wl, t, 74, "hybrid1", 1)
+    assert cfg["tile"] == [256, 256, 128] and cfg["tile_order"] == 16 and cfg["m"] == 8192
+    assert set(cfg) == {"workload", "m", "n", "k", "tile", "tile_order", "g", "policy", "parallelism"}
+
+
+def test_default_workload_is_cfg3_and_sweep_check_can_be_disabled():
+    import argparse  # noqa: F401
+
+    assert bench.WORKLOADS["cfg3"]["n"] == 14336
+    assert bench.sweep_check(1, 0, "none", bench.SWEEP_TILE) is None

@@ -173,6 +173,65 @@ def test_cuda_graph_replays_and_workspace_reuse():
             assert np.array_equal(p.c.double().cpu().numpy(), want)
 
 
+def test_graphs_captured_on_one_stream_replay_concurrently():
+    """Captured launches use a plan-private workspace (GemmPlan.prepare_for_capture), so two
+    graphs captured on the same stream can be replayed at the same time on two streams."""
+    m = sk()
+    rng = np.random.default_rng(9)
+    a = ogemm.random_int_matrix(512, 4096, rng)
+    b = ogemm.random_int_matrix(4096, 512, rng)
+    want = ogemm.reference_gemm(a, b)
+    at = torch.from_numpy(a).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(b).to(torch.bfloat16).cuda()
+    plans = [m.GemmPlan(at, bt, torch.zeros(512, 512, device="cuda"), m.Policy.all_stream_k(),
+                        m.TileShape(128, 128, 64)) for _ in range(2)]
+    side = torch.cuda.Stream()
+    graphs = []
+    for i, p in enumerate(plans):
+        if i == 0:
+            p.prepare_for_capture(side)  # the other plan allocates inside its capture
+        g = torch.cuda.CUDAGraph()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(4):
+                p.launch()
+        graphs.append(g)
+    assert plans[0]._private_ws.data_ptr() != plans[1]._private_ws.data_ptr()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    for _ in range(10):
+        for p in plans:
+            p.c.zero_()
+        torch.cuda.synchronize()
+        for g, s in zip(graphs, streams):
+            with torch.cuda.stream(s):
+                g.replay()
+        torch.cuda.synchronize()
+        for p in plans:
+            assert np.array_equal(p.c.double().cpu().numpy(), want)
+
+
+def test_first_launch_on_a_non_current_stream():
+    """The eager workspace of a new stream is allocated and zeroed on that stream, so a
+    plan launched with stream=s (s not torch's current stream) sees initialised flags."""
+    m = sk()
+    rng = np.random.default_rng(10)
+    a = ogemm.random_int_matrix(256, 8192, rng)
+    b = ogemm.random_int_matrix(8192, 384, rng)
+    want = ogemm.reference_gemm(a, b)
+    at = torch.from_numpy(a).to(torch.bfloat16).cuda()
+    bt = torch.from_numpy(b).to(torch.bfloat16).cuda()
+    for _ in range(3):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        c = torch.zeros(256, 384, device="cuda")
+        plan = m.GemmPlan(at, bt, c, m.Policy.all_stream_k(), m.TileShape(128, 128, 128))
+        for _ in range(3):
+            plan.launch(stream=s)
+        s.synchronize()
+        assert np.array_equal(c.double().cpu().numpy(), want)
+
+
 def test_device_schedule_trace_kernel_matches_host():
     m = sk()
     from paper_2408_11417_b200 import _lib, scheduler

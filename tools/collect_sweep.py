@@ -1,7 +1,9 @@
 #!/usr/bin/env python
-"""Copy a joint sweep (tools/gpurun_sweep_paper.sh -> gpurun_out/sweep_joint5/) into
-profiles/round1/sweep_joint5_*: per-tile records / validate / heldout CSVs, the summary,
-the per-size cost table and the tile bank (with its calibrated cost-model priors)."""
+"""Copy a joint sweep (e.g. tools/gpurun_sweep_r2.sh -> gpurun_out/sweep_r2/) into
+profiles/<round>/<prefix>_*: per-tile records and held-out CSVs (the validate pass is kept
+only as the summary's selection_heldout_run), the summary, the per-size cost table and the
+tile bank (with its calibrated cost-model priors); optionally install the bank as the
+package's shipped bank (paper_2408_11417_b200/banks/b200)."""
 import glob
 import os
 import shutil
@@ -10,11 +12,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def main(src="gpurun_out/sweep_joint5", prefix="sweep_joint5", bank="tilebank5"):
+def main(src="gpurun_out/sweep_r2", prefix="sweep_r2", bank="tilebank7", rnd="round2", install="1"):
     src = os.path.join(ROOT, src)
-    dst = os.path.join(ROOT, "profiles", "round1")
+    dst = os.path.join(ROOT, "profiles", rnd)
+    os.makedirs(dst, exist_ok=True)
     n = 0
-    for tag in ("records", "validate", "heldout"):
+    for tag in ("records", "heldout"):
         for p in glob.glob(os.path.join(src, f"{tag}.*.csv")):
             name = os.path.basename(p)
             if ".rank" in name:
@@ -29,7 +32,11 @@ def main(src="gpurun_out/sweep_joint5", prefix="sweep_joint5", bank="tilebank5")
     out_bank = os.path.join(dst, bank)
     shutil.rmtree(out_bank, ignore_errors=True)
     shutil.copytree(os.path.join(src, "tilebank"), out_bank)
-    print(f"copied {n} CSVs, summary, costs and {bank}/ into profiles/round1/")
+    if install == "1":
+        ship = os.path.join(ROOT, "paper_2408_11417_b200", "banks", "b200")
+        shutil.rmtree(ship, ignore_errors=True)
+        shutil.copytree(os.path.join(src, "tilebank"), ship)
+    print(f"copied {n} CSVs, summary, costs and {bank}/ into profiles/{rnd}/" + (" and installed the bank" if install == "1" else ""))
 
 
 if __name__ == "__main__":
