@@ -163,6 +163,10 @@ void skpp_debug_timeline(uint64_t* device_buffer);
    kernel runs its prologue (barriers, TMEM, descriptors) under that kernel's tail
    and waits (griddepcontrol.wait) before touching global memory. */
 void skpp_set_pdl(int enable);
+/* Cooperative launch of Stream-K grids (default on): the grid is gang-scheduled (all CTAs
+   resident or none), so reducers spinning on peer flags can never wait on a CTA that another
+   grid keeps off the SMs.  Data-parallel grids (no cross-CTA waits) are unaffected. */
+void skpp_set_cooperative(int enable);
 /* Load each stage's B columns with one 3-D TMA box when N % 64 == 0 (default on;
    plans created after the call). */
 void skpp_set_b3d(int enable);

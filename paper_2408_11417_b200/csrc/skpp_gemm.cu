@@ -1238,6 +1238,7 @@ static void sched_from_c(const skpp_sched_t& c, Sched& s) {
 
 static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
 static int g_pdl = 1;                    // skpp_set_pdl
+static int g_coop = 1;                   // skpp_set_cooperative
 static int g_b3d = 1;                    // skpp_set_b3d
 static int g_a3d = 1;                    // skpp_set_a3d
 static int g_l2_prefetch = 2;            // skpp_set_l2_prefetch (k-blocks)
@@ -1409,6 +1410,7 @@ extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_til
 
 extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
 extern "C" void skpp_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
+extern "C" void skpp_set_cooperative(int enable) { g_coop = enable ? 1 : 0; }
 extern "C" void skpp_set_b3d(int enable) { g_b3d = enable ? 1 : 0; }
 extern "C" void skpp_set_a3d(int enable) { g_a3d = enable ? 1 : 0; }
 extern "C" void skpp_set_l2_prefetch(int k_blocks) { g_l2_prefetch = k_blocks > 0 ? k_blocks : 0; }
@@ -1691,7 +1693,7 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = pl->smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[3];
+  cudaLaunchAttribute attr[4];
   cfg.attrs = attr;
   cfg.numAttrs = 0;
   if (g_pdl) {
@@ -1706,9 +1708,18 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
     attr[cfg.numAttrs].val.clusterDim.z = 1;
     ++cfg.numAttrs;
   }
-  // No cooperative attribute: no CTA waits before it has published all of its
-  // partials, and g never exceeds the co-resident CTAs (checked at plan time),
-  // so every waited-for CTA eventually runs; this keeps PDL overlap available.
+  // Liveness: phase-2 reducers spin on peer flags, so every CTA of a Stream-K grid
+  // must be resident at once.  g never exceeds the co-resident CTAs (checked at plan
+  // time), but that alone does not stop another grid (another stream, process or MPS
+  // client) from holding SMs while only part of this grid runs.  A cooperative launch
+  // makes the hardware gang-schedule the grid (all CTAs or none), so partially resident
+  // Stream-K grids — and the cross-grid deadlock they allow — cannot occur.
+  // Data-parallel grids have no cross-CTA waits and launch normally.
+  if (g_coop && pl->cs.sk_tiles > 0) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributeCooperative;
+    attr[cfg.numAttrs].val.cooperative = 1;
+    ++cfg.numAttrs;
+  }
   void* args[4] = {&pl->ma, &pl->mb, &pl->mc, &gp};
   cudaError_t e = cudaLaunchKernelExC(&cfg, pl->func, args);
   if (e != cudaSuccess) {

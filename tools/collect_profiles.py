@@ -30,9 +30,9 @@ def main(src="gpurun_out/prof", round_dir="profiles/round1"):
             json.dump(rows, fh, indent=1)
         with open(os.path.join(out, f"ncu_{wl}.json"), "w") as fh:
             json.dump(rows, fh, indent=1)
-    lp = os.path.join(src, "launches_cfg2.csv")
-    if os.path.exists(lp):
-        with open(os.path.join(out, "launches_cfg2.json"), "w") as fh:
+    for lp in glob.glob(os.path.join(src, "launches_*.csv")):
+        name = os.path.basename(lp)[:-4]
+        with open(os.path.join(out, f"{name}.json"), "w") as fh:
             json.dump(launches(lp), fh, indent=1)
     for f in glob.glob(os.path.join(src, "bench_*.json")):
         shutil.copy(f, out)

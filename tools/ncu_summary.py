@@ -68,7 +68,10 @@ def launches(path: str) -> dict:
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
         name = r["Kernel Name"]
-        short = "skpp::streamk_gemm" if "streamk_gemm" in name else name.split("(")[0][-60:]
+        if "streamk_gemm_kernel<" in name:  # per instantiation <BN, BK, CG, RASTER>
+            short = "streamk_gemm_kernel" + name[name.index("<"):name.index(">") + 1]
+        else:
+            short = name.split("(")[0][-60:]
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "ns")
         per.setdefault(short, []).append(v * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(unit, 1e-3))
