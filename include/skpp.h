@@ -163,9 +163,10 @@ void skpp_debug_timeline(uint64_t* device_buffer);
    kernel runs its prologue (barriers, TMEM, descriptors) under that kernel's tail
    and waits (griddepcontrol.wait) before touching global memory. */
 void skpp_set_pdl(int enable);
-/* Cooperative launch of Stream-K grids (default on): the grid is gang-scheduled (all CTAs
-   resident or none), so reducers spinning on peer flags can never wait on a CTA that another
-   grid keeps off the SMs.  Data-parallel grids (no cross-CTA waits) are unaffected. */
+/* Cooperative launch of Stream-K grids (default off).  Not needed for liveness: a phase-2
+   reducer waits for peer flags at most ~20 us, then hands its band to the tile's last
+   arriving contributor (abandon protocol, skpp_gemm.cu), so no CTA waits on a CTA that is
+   not resident.  Measured +14-17% per launch on small Stream-K shapes (no PDL overlap). */
 void skpp_set_cooperative(int enable);
 /* Load each stage's B columns with one 3-D TMA box when N % 64 == 0 (default on;
    plans created after the call). */
@@ -182,8 +183,14 @@ void skpp_set_l2_prefetch(int k_blocks);
 void skpp_set_l2_hints(int enable);
 /* Test hooks (plans created after the call): bit 0 forces the two-pass Stream-K fixup
    (peers first, owner added in a second pass) even when the owner is already published;
-   results are bit-identical to the one-pass path by construction (tests check it). */
+   bit 1 sets the phase-2 wait bound to 0, so every band whose flags are not already up is
+   abandoned and reduced by the tile's last arriver or reclaimed by its reducer; results
+   are bit-identical to the normal path by construction (tests check it). */
 void skpp_set_debug(int flags);
+/* Test hook for the liveness tests: launch `ctas` single-warp CTAs with `smem_bytes` of
+   dynamic shared memory each that occupy their SMs until *release != 0 (bounded at ~35 s),
+   so a Stream-K grid launched next on another stream is only partially resident. */
+int skpp_test_hold_sms(uint32_t ctas, uint32_t smem_bytes, const uint32_t* release, void* stream);
 /* SM count, compute capability and the co-resident CTA limit of the GEMM kernel for blk_n. */
 int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 int skpp_max_coresident(const skpp_tile_t* t, int32_t* ctas);

@@ -137,6 +137,7 @@ SIGNATURES = {
     "skpp_debug_timeline": (None, [C.c_void_p]),
     "skpp_set_pdl": (None, [C.c_int]),
     "skpp_set_cooperative": (None, [C.c_int]),
+    "skpp_test_hold_sms": (C.c_int, [C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "skpp_set_b3d": (None, [C.c_int]),
     "skpp_set_a3d": (None, [C.c_int]),
     "skpp_set_l2_prefetch": (None, [C.c_int]),

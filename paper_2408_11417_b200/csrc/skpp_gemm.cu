@@ -52,9 +52,23 @@ constexpr int kEpiWarp0 = 4;
 constexpr uint32_t kRingBudget = 196608;   // operand ring (192 KiB)
 constexpr uint32_t kStageBuf = 4096;       // one epilogue staging buffer: 32 rows x 128 B
 constexpr uint32_t kStagingBytes = 4 * 2 * kStageBuf;
-// Workspace: [256 B header][2g flags, 256-B rounded][2g slots x BM x BN fp32]
-constexpr uint64_t kWsHeader = 256;
-inline uint64_t ws_flag_bytes(uint64_t g) { return (2 * g * 4 + 255) / 256 * 256; }
+// Workspace: a fixed 32 KiB control block, then 2 slots of BM x BN fp32 per CTA.
+//   [0, 256)          header: [0] epoch of the last completed Stream-K launch, [1] arrivals
+//   [1 KiB, 9 KiB)    slot flags, 2 per CTA (== epoch when the slot holds this launch's partial)
+//   [9 KiB, 17 KiB)   arrival tickets [2 parities][kMaxCtas]: per split tile (indexed by its
+//                     first contributor), low 16 bits = contributors that published, high 16 =
+//                     reducers that gave up waiting (see phase 2)
+//   [17 KiB, 25 KiB)  band states [2 parities][kMaxCtas] per reducing CTA: 0 none,
+//                     1 abandoned, 2 claimed by the tile's last arriver, 3 reclaimed by the reducer
+// Fixed offsets: plans of any grid size share one workspace without their control words
+// ever overlapping another plan's partial slots.  Launch e uses the parity e & 1 arrays and
+// zeroes the other parity's for launch e + 1 (which starts only after this grid completed).
+constexpr uint32_t kMaxCtas = 1024;
+constexpr uint64_t kWsFlagsOff = 1024;
+constexpr uint64_t kWsTicketsOff = kWsFlagsOff + 2ull * kMaxCtas * 4;
+constexpr uint64_t kWsStatesOff = kWsTicketsOff + 2ull * kMaxCtas * 4;
+constexpr uint64_t kWsCtlBytes = 32768;
+static_assert(kWsStatesOff + 2ull * kMaxCtas * 4 <= kWsCtlBytes, "workspace control block");
 
 #ifndef SKPP_WATCHDOG_CYCLES
 #define SKPP_WATCHDOG_CYCLES (1ull << 35)  // ~17 s at 1.9 GHz: trap instead of hanging
@@ -298,6 +312,16 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t atom_cas_acq_rel_gpu(uint32_t* p, uint32_t cmp, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ float4 ld_cg_f4(const float4* p) {
   float4 v;
   asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -347,7 +371,7 @@ struct Cfg {
                                         : 2 * BN <= 128 ? 128
                                         : 2 * BN <= 256 ? 256
                                                         : 512;
-  static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 48 + 1023) / 1024 * 1024;
+  static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 224 + 1023) / 1024 * 1024;
   static constexpr uint32_t SMEM = RING_BYTES + kStagingBytes + BAR_BYTES + 1024;
   // A: K-major, one swizzle atom along K (BK*2 bytes = 32/64/128 B)
   // BK = 128: two SW128 sub-tiles of [128 rows][64 k] (one TMA box each, 16 KiB apart)
@@ -378,6 +402,9 @@ struct GemmParams {
   float* ws;           // 2g partial slots of BM x BN fp32, row-major
   uint32_t* flags;     // 2g slot flags (== epoch when the slot holds this launch's partial)
   uint32_t* hdr;       // [0] epoch of the last completed launch, [1] CTAs of this launch that read [0]
+  uint32_t* tickets;   // [2][kMaxCtas] arrival tickets (parity = epoch & 1)
+  uint32_t* bstate;    // [2][kMaxCtas] band states of the reducing CTAs
+  uint32_t abandon_cycles;  // phase-2 flag wait before a reducer hands its band to the last arriver
   int64_t* trace;
   uint64_t trace_cap;
   int64_t* trace_counts;
@@ -387,7 +414,9 @@ struct GemmParams {
   uint32_t a_tx;        // A bytes per stage per CTA (the A box covers round_up(M, 8) rows when M < 128)
   uint32_t l2_prefetch; // k-blocks of the first item prefetched to L2 before griddepcontrol.wait
   uint32_t l2_hints;    // B loads evict_last, C stores evict_first (skpp_set_l2_hints)
-  uint32_t debug;       // skpp_set_debug: bit 0 = always take the two-pass (owner-late) fixup path
+  uint32_t debug;       // skpp_set_debug: bit 0 = always take the two-pass (owner-late) fixup path,
+                        // bit 1 = abandon at once (every band whose flags are not already up goes
+                        // through the abandon / last-arriver path)
   uint32_t raster;      // tile order: 0 = row-major (reference), G = bands of G tile rows (tile_rc)
   uint32_t ragged;      // last row / column tile at most half full: partials and bands skip rows >= M, cols >= N
 };
@@ -511,6 +540,17 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t epoch) 
     __nanosleep(32);
     watchdog(t0, 5);
   }
+}
+
+// Bounded flag wait of phase 2: true when the flag shows this launch's epoch before
+// `cycles` SM cycles have passed since t0.
+__device__ __forceinline__ bool wait_flag_until(const uint32_t* flag, uint32_t epoch, long long t0,
+                                                uint32_t cycles) {
+  while (ld_acquire_gpu(flag) != epoch) {
+    if (clock64() - t0 > (long long)cycles) return false;
+    __nanosleep(32);
+  }
+  return true;
 }
 
 // Phase 2 works on a BAND of rows of the split tile: reducer idx of nr owns rows
@@ -656,9 +696,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* split_smem = red_bar + 2;                       // phase-2 work list (2 tiles)
   uint32_t* nsplit_smem = reinterpret_cast<uint32_t*>(red_bar + 4);
 
+  // phase-2 scratch words (after nsplit_smem[0] n_split, [2] peers seen, [3] epoch):
+  // [1] abandon / hand-off decision, [4] [5] split tiles of the pending ticket arrivals,
+  // [6] which arrivals were issued, [7] owner ready, [8] last-arriver work, [9..41) claim bitmask
+  uint32_t* ctl_smem = nsplit_smem;
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // row half of the pair tile
+  // Ticket arrivals of this CTA's (<= 2) partial items, issued by the epilogue leader right
+  // after each flag release; the returned counts are consumed only at the end of phase 2.
+  uint32_t pend_old0 = 0, pend_old1 = 0;
   const uint32_t x = blockIdx.x / CG;                      // workgroup (pair) id
   const Sched& s = p.s;
 
@@ -899,6 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_c = l2_policy_evict_first();
     uint64_t split_tiles[1];
     uint32_t n_split = 0, sk_seen = 0, local = 0;
+    if (leader) ctl_smem[6] = 0u;  // which of the two pending arrivals were issued
     Cursor cur;
     cursor_init(cur, s, x);
     Item it;
@@ -973,6 +1021,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           st_release_gpu(p.flags + slot, epoch);
+          // Arrival ticket of the split tile (indexed by its first contributor x0): the
+          // deadlock-free fallback of phase 2 (a reducer that gives up waiting leaves its band
+          // to the tile's last arriver).  Issued after the flag release (acq_rel: ordered
+          // after it), not waited on here.
+          const uint64_t uu = it.tile - s.dp_tiles;
+          const uint64_t x0u = (uu * s.ipt) / s.ipw;
+          const uint32_t old = atom_add_acq_rel_gpu(p.tickets + (epoch & 1u) * kMaxCtas + x0u * CG + rank, 1u);
+          if (sk_seen == 0) pend_old0 = old; else pend_old1 = old;
+          ctl_smem[4 + (sk_seen == 0 ? 0 : 1)] = (uint32_t)uu;
+          ctl_smem[6] |= sk_seen == 0 ? 1u : 2u;
         }
         if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_FLAG);
         // the CTA reduces (phase 2) only the tile of its FIRST Stream-K item
@@ -1103,41 +1161,157 @@ __global__ void __launch_bounds__(kThreads, 1)
                           p.timeline ? p.timeline + (uint64_t)blockIdx.x * TL_EVENTS : nullptr};
       const uint32_t stage = smem_u32(smem);  // idle operand ring: float4 [row][V+1]
       // Peer flags are awaited by one thread each; thread kThreads-1 polls the
-      // owner's flag until either it is up or every peer has been seen.
-      if (ft == 0) *peers_seen = 0u;
+      // owner's flag until either it is up or every peer has been seen.  Every wait is
+      // bounded by p.abandon_cycles: a contributor that has not published by then may not
+      // be resident (another grid holding SMs), so this reducer hands its band to the
+      // tile's last arriver instead of spinning (abandon protocol below).
+      if (ft == 0) {
+        *peers_seen = 0u;
+        ctl_smem[1] = 0u;  // abandon requested
+      }
       phase2_bar_sync();
+      const long long wait_t0 = clock64();
       if (ft < kThreads - 1) {
         for (uint32_t t = 1 + ft; t < nc; t += kThreads - 1) {
-          wait_flag(p.flags + 2 * ((x0 + t) * CG + rank), epoch);
+          if (!wait_flag_until(p.flags + 2 * ((x0 + t) * CG + rank), epoch, wait_t0, p.abandon_cycles)) {
+            ctl_smem[1] = 1u;
+            break;
+          }
           atomicAdd(const_cast<uint32_t*>(peers_seen), 1u);
         }
       }
       if (ft == kThreads - 1) {
         const uint32_t want = nc - 1;
         uint32_t ready = 0;
-        const long long t0 = clock64();
         while (true) {
           if (ld_acquire_gpu(p.flags + slot0) == epoch) { ready = 1; break; }
           if (*peers_seen >= want) break;
-          watchdog(t0, 6);
+          if (*reinterpret_cast<volatile uint32_t*>(ctl_smem + 1) != 0u ||
+              clock64() - wait_t0 > (long long)p.abandon_cycles) {
+            ctl_smem[1] = 1u;
+            break;
+          }
         }
-        nsplit_smem[1] = ready;
+        ctl_smem[7] = ready;
       }
       phase2_bar_sync();
+      bool owner_ready = ctl_smem[7] != 0 && !(p.debug & 1u);
+      if (ctl_smem[1] != 0u) {
+        // Abandon protocol (thread 0): mark the band abandoned, then register on the tile's
+        // ticket.  If every contributor has arrived by then, take the band back and reduce
+        // it now (exactly one of this CAS and the last arriver's claim succeeds); otherwise
+        // the last arriver — which sees this abandonment on the ticket — reduces it.
+        if (ft == 0) {
+          uint32_t* st = p.bstate + (epoch & 1u) * kMaxCtas + (x * CG + rank);
+          atom_cas_acq_rel_gpu(st, 0u, 1u);
+          const uint32_t tk = atom_add_acq_rel_gpu(p.tickets + (epoch & 1u) * kMaxCtas + x0 * CG + rank, 1u << 16);
+          uint32_t mine = 0;
+          if ((tk & 0xFFFFu) == nc && atom_cas_acq_rel_gpu(st, 1u, 3u) == 1u) mine = 1;
+          ctl_smem[1] = mine ? 2u : 3u;
+        }
+        phase2_bar_sync();
+        if (ctl_smem[1] == 3u) {
+          phase2_bar_sync();  // ctl_smem[1] is rewritten by the next split tile
+          continue;           // the last arriver reduces this band
+        }
+        owner_ready = !(p.debug & 1u);  // every contributor has published
+      }
       if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
-      const bool owner_ready = nsplit_smem[1] != 0 && !(p.debug & 1u);
       const uint32_t nrows = R1 - R0;
       band_reduce<CG, V>(ra, R0, nrows, Vv, 0, owner_ready ? nc : nc - 1, false, stage, ft);
       if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM1);
       if (!owner_ready) {
-        if (ft == 0) wait_flag(p.flags + slot0, epoch);
+        // the owner's flag (every peer has published); bounded like the waits above
+        if (ft == 0) {
+          uint32_t ok = wait_flag_until(p.flags + slot0, epoch, clock64(), p.abandon_cycles) ? 1u : 0u;
+          if (!ok) {
+            uint32_t* st = p.bstate + (epoch & 1u) * kMaxCtas + (x * CG + rank);
+            atom_cas_acq_rel_gpu(st, 0u, 1u);
+            const uint32_t tk = atom_add_acq_rel_gpu(p.tickets + (epoch & 1u) * kMaxCtas + x0 * CG + rank, 1u << 16);
+            ok = ((tk & 0xFFFFu) == nc && atom_cas_acq_rel_gpu(st, 1u, 3u) == 1u) ? 1u : 0u;
+          }
+          ctl_smem[1] = ok;
+        }
         phase2_bar_sync();  // also orders the stage writes above before the re-reads below
+        if (ctl_smem[1] == 0u) {
+          phase2_bar_sync();
+          continue;  // handed to the last arriver
+        }
         band_reduce<CG, V>(ra, R0, nrows, Vv, nc - 1, nc, true, stage, ft);
         if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM2);
       }
       phase2_bar_sync();
       band_store<V>(p, stage, nrows, Vv, row0, gcol0, ft);
       phase2_bar_sync();  // stage and nsplit_smem[1..2] are reused by the next split tile
+    }
+    // ---- last arriver: reduce the bands whose reducers gave up before the tile's last
+    // arrival.  The leader's ticket arrivals (phase 1) returned (abandons << 16 | earlier
+    // arrivals); the arrival that completed a tile (earlier arrivals + 1 == nc) with
+    // abandons > 0 claims every band still marked abandoned (CAS 1 -> 2; a reducer that
+    // abandoned after this arrival saw the full count and took its band back, CAS 1 -> 3).
+    // Normally nothing is abandoned: one barrier, no memory traffic.
+    if (ft == kEpiWarp0 * 32) {
+      uint32_t todo = 0;
+      const uint32_t valid = ctl_smem[6];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (!(valid >> j & 1u)) continue;
+        const uint32_t old = j == 0 ? pend_old0 : pend_old1;
+        const uint64_t u = ctl_smem[4 + j];
+        const uint64_t x0 = (u * s.ipt) / s.ipw, x1 = ((u + 1) * s.ipt - 1) / s.ipw;
+        if ((old & 0xFFFFu) + 1u == (uint32_t)(x1 - x0 + 1) && (old >> 16) != 0u) todo |= 1u << j;
+      }
+      ctl_smem[8] = todo;
+    }
+    phase2_bar_sync();
+    const uint32_t todo = ctl_smem[8];
+    for (int j = 0; j < 2; ++j) {
+      if (!(todo >> j & 1u)) continue;
+      const uint64_t u = ctl_smem[4 + j];
+      const uint64_t x0 = (u * s.ipt) / s.ipw, x1 = ((u + 1) * s.ipt - 1) / s.ipw;
+      const uint32_t nc = (uint32_t)(x1 - x0 + 1);
+      const bool aligned = x0 * s.ipw == u * s.ipt;
+      const uint64_t r_lo = x0 + (aligned ? 0 : 1);
+      const uint32_t nr = (uint32_t)(x1 - r_lo + 1);
+      uint32_t* mask = ctl_smem + 9;
+      if (ft < 32) mask[ft] = 0u;
+      phase2_bar_sync();
+      for (uint32_t i = ft; i < nr; i += kThreads) {
+        uint32_t* st = p.bstate + (epoch & 1u) * kMaxCtas + (r_lo + i) * CG + rank;
+        if (ld_acquire_gpu(st) == 1u && atom_cas_acq_rel_gpu(st, 1u, 2u) == 1u) atomicOr(mask + (i >> 5), 1u << (i & 31));
+      }
+      phase2_bar_sync();
+      uint32_t rows_ok = kBM, Vv = V;
+      uint64_t utm, utn;
+      tile_rc<RASTER>(s, p.raster, s.dp_tiles + u, utm, utn);
+      if (p.ragged) {
+        const uint64_t tile_rows0 = utm * TILE_M + rank * kBM;
+        rows_ok = tile_rows0 >= p.M ? 0u : (p.M - tile_rows0 < (uint64_t)kBM ? (uint32_t)(p.M - tile_rows0) : kBM);
+        const uint64_t tile_cols0 = utn * BN;
+        if (p.N - tile_cols0 < (uint64_t)BN) Vv = (uint32_t)((p.N - tile_cols0 + 31) / 32 * 32 / 4);
+      }
+      const uint64_t slot0 = 2 * (x0 * CG + rank) + (aligned ? 0 : 1);
+      const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc, nullptr};
+      const uint32_t stage = smem_u32(smem);
+      for (uint32_t idx = 0; idx < nr; ++idx) {
+        if (!(mask[idx >> 5] >> (idx & 31) & 1u)) continue;
+        const uint32_t R0 = (uint32_t)(((uint64_t)idx * rows_ok) / nr);
+        const uint32_t R1 = (uint32_t)(((uint64_t)(idx + 1) * rows_ok) / nr);
+        if (R0 == R1) continue;
+        band_reduce<CG, V>(ra, R0, R1 - R0, Vv, 0, nc, false, stage, ft);
+        phase2_bar_sync();
+        band_store<V>(p, stage, R1 - R0, Vv, utm * TILE_M + rank * kBM + R0, utn * BN, ft);
+        phase2_bar_sync();
+      }
+    }
+    // Zero the other parity's tickets and band states for the next Stream-K launch on
+    // this workspace (it starts touching them only after this grid has completed).
+    if (ft < 32) {
+      const uint32_t np = (epoch & 1u) ^ 1u;
+      for (uint32_t i = blockIdx.x + gridDim.x * ft; i < kMaxCtas; i += 32 * gridDim.x) {
+        p.tickets[np * kMaxCtas + i] = 0u;
+        p.bstate[np * kMaxCtas + i] = 0u;
+      }
     }
     if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
   }
@@ -1159,6 +1333,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                    "n"(C::TMEM_COLS)
                    : "memory");
   }
+}
+
+// Test hook (skpp_test_hold_sms): CTAs that occupy SMs until *release != 0 (or ~35 s).
+__global__ void hold_sms_kernel(const volatile uint32_t* release) {
+  if (threadIdx.x != 0) return;
+  const long long t0 = clock64();
+  while (*release == 0u && clock64() - t0 < (1ll << 36)) __nanosleep(2000);
 }
 
 // Decode-only: every CTA walks its items with the same cursor and records them.
@@ -1238,7 +1419,7 @@ static void sched_from_c(const skpp_sched_t& c, Sched& s) {
 
 static uint64_t* g_timeline = nullptr;  // skpp_debug_timeline
 static int g_pdl = 1;                    // skpp_set_pdl
-static int g_coop = 1;                   // skpp_set_cooperative
+static int g_coop = 0;                   // skpp_set_cooperative
 static int g_b3d = 1;                    // skpp_set_b3d
 static int g_a3d = 1;                    // skpp_set_a3d
 static int g_l2_prefetch = 2;            // skpp_set_l2_prefetch (k-blocks)
@@ -1405,7 +1586,7 @@ extern "C" uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_til
   if (!t) return 0;
   // two partial slots (first / last Stream-K item) of 128 x blk_n fp32 per CTA
   const uint64_t ctas = (uint64_t)g * (t->blk_m > (uint32_t)kBM ? 2 : 1);
-  return kWsHeader + ws_flag_bytes(ctas) + 2ull * ctas * kBM * t->blk_n * 4;
+  return kWsCtlBytes + 2ull * ctas * kBM * t->blk_n * 4;
 }
 
 extern "C" void skpp_debug_timeline(uint64_t* device_buffer) { g_timeline = device_buffer; }
@@ -1434,6 +1615,23 @@ extern "C" int skpp_stream_is_capturing(void* stream) {
     return SKPP_ELAUNCH;
   }
   return st == cudaStreamCaptureStatusActive ? 1 : 0;
+}
+
+extern "C" int skpp_test_hold_sms(uint32_t ctas, uint32_t smem_bytes, const uint32_t* release, void* stream) {
+  if (!release || ctas == 0) {
+    set_error("hold_sms: null release flag or no CTAs");
+    return SKPP_EINVAL;
+  }
+  cudaError_t e = cudaFuncSetAttribute(hold_sms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+  if (e == cudaSuccess) {
+    hold_sms_kernel<<<ctas, 32, smem_bytes, reinterpret_cast<cudaStream_t>(stream)>>>(release);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    set_error(std::string("hold_sms launch: ") + cudaGetErrorString(e));
+    return SKPP_ELAUNCH;
+  }
+  return SKPP_OK;
 }
 
 extern "C" int skpp_device_info(int device, int32_t* sm_count, int32_t* cc_major,
@@ -1630,6 +1828,9 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
   }
   gp.l2_hints = g_l2_hints ? 1 : 0;
   gp.debug = (uint32_t)g_debug;
+  // ~20 us at 1.9 GHz: far above any wait of a fully resident grid (flags trail the mainloop
+  // by ~1-3 us), short enough that a reducer blocked by a non-resident peer frees its SM soon
+  gp.abandon_cycles = (g_debug & 2) ? 0u : 40000u;
   // Skip-invalid-rows/columns mode only where it saves at least half a tile of partial
   // bytes (decode-like M, narrow N): on other shapes the bounds checks cost more than the
   // 32-row / 32-column chunks they would skip.
@@ -1680,8 +1881,10 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
     if (pl->ws_bound != workspace) {
       uint8_t* base = reinterpret_cast<uint8_t*>(workspace);
       gp.hdr = reinterpret_cast<uint32_t*>(base);
-      gp.flags = reinterpret_cast<uint32_t*>(base + kWsHeader);
-      gp.ws = reinterpret_cast<float*>(base + kWsHeader + ws_flag_bytes((uint64_t)pl->cs.g * pl->cg));
+      gp.flags = reinterpret_cast<uint32_t*>(base + kWsFlagsOff);
+      gp.tickets = reinterpret_cast<uint32_t*>(base + kWsTicketsOff);
+      gp.bstate = reinterpret_cast<uint32_t*>(base + kWsStatesOff);
+      gp.ws = reinterpret_cast<float*>(base + kWsCtlBytes);
       pl->ws_bound = workspace;
     }
   }

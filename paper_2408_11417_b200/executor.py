@@ -136,7 +136,7 @@ def tile_supported(tile: TileShape) -> bool:
     return bool(_lib.lib.skpp_tile_supported(_lib.tile_c(tile)))
 
 
-WS_ZERO_BYTES = 4096  # header (256 B) + the flags of up to 2 x 148 CTAs, 256-B rounded, with margin
+WS_ZERO_BYTES = 32768  # the control block: header, flags, tickets and band states (skpp_gemm.cu)
 
 
 def _new_workspace(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
