@@ -164,9 +164,10 @@ void skpp_debug_timeline(uint64_t* device_buffer);
    and waits (griddepcontrol.wait) before touching global memory. */
 void skpp_set_pdl(int enable);
 /* Cooperative launch of Stream-K grids (default off).  Not needed for liveness: a phase-2
-   reducer waits for peer flags at most ~20 us, then hands its band to the tile's last
-   arriving contributor (abandon protocol, skpp_gemm.cu), so no CTA waits on a CTA that is
-   not resident.  Measured +14-17% per launch on small Stream-K shapes (no PDL overlap). */
+   reducer that waits ~20 us for peer flags keeps waiting only if every CTA of the launch has
+   started, else it abandons its band to the last CTA to start (skpp_gemm.cu, phase 2), so no
+   CTA waits on a CTA that is not resident.  Measured +12-23% per launch on small Stream-K
+   shapes (a cooperative grid gets no PDL overlap). */
 void skpp_set_cooperative(int enable);
 /* Load each stage's B columns with one 3-D TMA box when N % 64 == 0 (default on;
    plans created after the call). */
@@ -183,9 +184,9 @@ void skpp_set_l2_prefetch(int k_blocks);
 void skpp_set_l2_hints(int enable);
 /* Test hooks (plans created after the call): bit 0 forces the two-pass Stream-K fixup
    (peers first, owner added in a second pass) even when the owner is already published;
-   bit 1 sets the phase-2 wait bound to 0, so every band whose flags are not already up is
-   abandoned and reduced by the tile's last arriver or reclaimed by its reducer; results
-   are bit-identical to the normal path by construction (tests check it). */
+   bit 1 sets the phase-2 wait bound to 0, so every wait not already satisfied takes the
+   timeout decision (keep waiting if every CTA started, else abandon to the last starter);
+   results are bit-identical to the normal path by construction (tests check it). */
 void skpp_set_debug(int flags);
 /* Test hook for the liveness tests: launch `ctas` single-warp CTAs with `smem_bytes` of
    dynamic shared memory each that occupy their SMs until *release != 0 (bounded at ~35 s),

@@ -7,6 +7,7 @@ loaded, importing the package raises, so nothing silently runs on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from . import _build
@@ -183,15 +184,21 @@ SIGNATURES = {
 
 
 def _load() -> C.CDLL:
-    if _build.is_stale():
+    # Development hook for same-box A/B runs of two kernel builds (tools/ab_libs.py):
+    # SKPP_LIB names another build of libskpp.so; entry points it lacks stay unbound.
+    override = os.environ.get("SKPP_LIB")
+    if not override and _build.is_stale():
         # In-tree sources are newer than the library (or it is missing): rebuild.
         # On a box without nvcc this raises, which is the intended loud failure.
         _build.build()
+    path = override or str(LIB_PATH)
     try:
-        lib = C.CDLL(str(LIB_PATH))
+        lib = C.CDLL(path)
     except OSError as exc:  # pragma: no cover - exercised only on broken installs
-        raise ImportError(f"cannot load {LIB_PATH}: {exc}") from exc
+        raise ImportError(f"cannot load {path}: {exc}") from exc
     for name, (res, args) in SIGNATURES.items():
+        if override and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

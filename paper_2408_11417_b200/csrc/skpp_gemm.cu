@@ -53,20 +53,17 @@ constexpr uint32_t kRingBudget = 196608;   // operand ring (192 KiB)
 constexpr uint32_t kStageBuf = 4096;       // one epilogue staging buffer: 32 rows x 128 B
 constexpr uint32_t kStagingBytes = 4 * 2 * kStageBuf;
 // Workspace: a fixed 32 KiB control block, then 2 slots of BM x BN fp32 per CTA.
-//   [0, 256)          header: [0] epoch of the last completed Stream-K launch, [1] arrivals
+//   [0, 256)          header: [0] epoch of the last completed Stream-K launch, [1] arrivals,
+//                     [8 + par] CTAs started, [16 + par] abandoned bands (phase 2, par = epoch & 1)
 //   [1 KiB, 9 KiB)    slot flags, 2 per CTA (== epoch when the slot holds this launch's partial)
-//   [9 KiB, 17 KiB)   arrival tickets [2 parities][kMaxCtas]: per split tile (indexed by its
-//                     first contributor), low 16 bits = contributors that published, high 16 =
-//                     reducers that gave up waiting (see phase 2)
-//   [17 KiB, 25 KiB)  band states [2 parities][kMaxCtas] per reducing CTA: 0 none,
-//                     1 abandoned, 2 claimed by the tile's last arriver, 3 reclaimed by the reducer
+//   [9 KiB, 17 KiB)   band states [2 parities][kMaxCtas] per reducing CTA: 0 none,
+//                     1 abandoned, 2 claimed by the last-starting CTA, 3 taken back
 // Fixed offsets: plans of any grid size share one workspace without their control words
-// ever overlapping another plan's partial slots.  Launch e uses the parity e & 1 arrays and
-// zeroes the other parity's for launch e + 1 (which starts only after this grid completed).
+// ever overlapping another plan's partial slots.  Launch e uses the parity e & 1 words and
+// resets the other parity's for launch e + 1 (which starts only after this grid completed).
 constexpr uint32_t kMaxCtas = 1024;
 constexpr uint64_t kWsFlagsOff = 1024;
-constexpr uint64_t kWsTicketsOff = kWsFlagsOff + 2ull * kMaxCtas * 4;
-constexpr uint64_t kWsStatesOff = kWsTicketsOff + 2ull * kMaxCtas * 4;
+constexpr uint64_t kWsStatesOff = kWsFlagsOff + 2ull * kMaxCtas * 4;
 constexpr uint64_t kWsCtlBytes = 32768;
 static_assert(kWsStatesOff + 2ull * kMaxCtas * 4 <= kWsCtlBytes, "workspace control block");
 
@@ -371,7 +368,7 @@ struct Cfg {
                                         : 2 * BN <= 128 ? 128
                                         : 2 * BN <= 256 ? 256
                                                         : 512;
-  static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 224 + 1023) / 1024 * 1024;
+  static constexpr uint32_t BAR_BYTES = ((2 * STAGES + 5) * 8 + 32 + 16 * 4 + 1023) / 1024 * 1024;
   static constexpr uint32_t SMEM = RING_BYTES + kStagingBytes + BAR_BYTES + 1024;
   // A: K-major, one swizzle atom along K (BK*2 bytes = 32/64/128 B)
   // BK = 128: two SW128 sub-tiles of [128 rows][64 k] (one TMA box each, 16 KiB apart)
@@ -402,9 +399,8 @@ struct GemmParams {
   float* ws;           // 2g partial slots of BM x BN fp32, row-major
   uint32_t* flags;     // 2g slot flags (== epoch when the slot holds this launch's partial)
   uint32_t* hdr;       // [0] epoch of the last completed launch, [1] CTAs of this launch that read [0]
-  uint32_t* tickets;   // [2][kMaxCtas] arrival tickets (parity = epoch & 1)
-  uint32_t* bstate;    // [2][kMaxCtas] band states of the reducing CTAs
-  uint32_t abandon_cycles;  // phase-2 flag wait before a reducer hands its band to the last arriver
+  uint32_t* bstate;    // [2][kMaxCtas] band states of the reducing CTAs (parity = epoch & 1)
+  uint32_t abandon_cycles;  // phase-2 flag wait before a reducer checks whether every CTA started
   int64_t* trace;
   uint64_t trace_cap;
   int64_t* trace_counts;
@@ -430,6 +426,7 @@ enum : int {
   TL_PHASE1 = 4,      // epilogue finished all items (stores / partials)
   TL_WAITED = 5,      // epilogue finished waiting for the first split tile's flags
   TL_PHASE2 = 6,      // epilogue finished the reductions
+  TL_END = 7,         // every warp done (the last starter's cleanup included)
   TL_EPI_FIRST = 8,   // epilogue saw its first accumulator
   TL_PART_ISSUED = 9, // first partial: all TMA stores issued
   TL_PART_FLAG = 10,  // first partial: flag released
@@ -551,6 +548,25 @@ __device__ __forceinline__ bool wait_flag_until(const uint32_t* flag, uint32_t e
     __nanosleep(32);
   }
   return true;
+}
+
+// Header words of the liveness protocol (phase 2), per parity of the launch epoch.
+constexpr uint32_t kHdrStarted = 8;   // hdr[8 + par]: CTAs of the launch that have started
+constexpr uint32_t kHdrAbandon = 16;  // hdr[16 + par]: some band of the launch was abandoned
+
+// A phase-2 flag wait timed out (thread 0).  Returns 1 to keep waiting, 0 when the band was
+// handed to the launch's last-starting CTA.  If every CTA has started, every partial will
+// be published: keep waiting.  Otherwise mark the band abandoned (state 1) and flag the
+// launch, then look again: if the last CTA started meanwhile it may have missed the mark,
+// so take the band back (CAS 1 -> 3; the last starter claims with CAS 1 -> 2, exactly one
+// succeeds).  The RMW reads of the counter order the marks before any later start.
+__device__ __noinline__ uint32_t abandon_or_wait(uint32_t* hdr, uint32_t par, uint32_t* bst) {
+  if (atom_add_acq_rel_gpu(hdr + kHdrStarted + par, 0u) >= gridDim.x) return 1u;
+  atom_cas_acq_rel_gpu(bst, 0u, 1u);
+  atom_add_acq_rel_gpu(hdr + kHdrAbandon + par, 1u);
+  if (atom_add_acq_rel_gpu(hdr + kHdrStarted + par, 0u) >= gridDim.x && atom_cas_acq_rel_gpu(bst, 1u, 3u) == 1u)
+    return 1u;
+  return 0u;
 }
 
 // Phase 2 works on a BAND of rows of the split tile: reducer idx of nr owns rows
@@ -678,7 +694,7 @@ template <int BN, int BK, int CG, bool RASTER = false>
 __global__ void __launch_bounds__(kThreads, 1)
     streamk_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmC, const __grid_constant__ GemmParams p) {
   using C = Cfg<BN, BK, CG>;
   constexpr uint32_t TILE_M = kBM * CG;
   extern __shared__ uint8_t smem_raw[];
@@ -696,16 +712,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* split_smem = red_bar + 2;                       // phase-2 work list (2 tiles)
   uint32_t* nsplit_smem = reinterpret_cast<uint32_t*>(red_bar + 4);
 
-  // phase-2 scratch words (after nsplit_smem[0] n_split, [2] peers seen, [3] epoch):
-  // [1] abandon / hand-off decision, [4] [5] split tiles of the pending ticket arrivals,
-  // [6] which arrivals were issued, [7] owner ready, [8] last-arriver work, [9..41) claim bitmask
-  uint32_t* ctl_smem = nsplit_smem;
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // row half of the pair tile
-  // Ticket arrivals of this CTA's (<= 2) partial items, issued by the epilogue leader right
-  // after each flag release; the returned counts are consumed only at the end of phase 2.
-  uint32_t pend_old0 = 0, pend_old1 = 0;
+
   const uint32_t x = blockIdx.x / CG;                      // workgroup (pair) id
   const Sched& s = p.s;
 
@@ -721,6 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty_bar[i], 4 * CG);  // every epilogue warp of the pair
     }
     mbar_init(red_bar, 1);
+    nsplit_smem[4] = 0u;  // last-starter cleanup (set by the epilogue leader)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_shared();
   }
@@ -940,13 +951,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.hdr[1] = 0u;
         p.hdr[0] = epoch;
       }
+      // liveness protocol (phase 2): count this CTA as started; the last one to start
+      // learns here whether any band was abandoned before it started (none can be after)
+      const uint32_t par = epoch & 1u, np = par ^ 1u;
+      uint32_t cleanup = 0;
+      if (atom_add_acq_rel_gpu(p.hdr + kHdrStarted + par, 1u) == gridDim.x - 1)
+        cleanup = ld_acquire_gpu(p.hdr + kHdrAbandon + par) != 0u ? 1u : 0u;
+      nsplit_smem[4] = cleanup;
+      // reset the other parity's words for the next Stream-K launch on this workspace
+      // (it touches them only after this grid has completed)
+      for (uint32_t i = blockIdx.x; i < kMaxCtas; i += gridDim.x) p.bstate[np * kMaxCtas + i] = 0u;
+      if (blockIdx.x == 0) {
+        p.hdr[kHdrStarted + np] = 0u;
+        p.hdr[kHdrAbandon + np] = 0u;
+      }
     }
     const uint32_t stg_base = smem_u32(stg) + ew * 2 * kStageBuf;
     uint32_t sbuf = 0;  // staging buffer toggle of this warp
     const uint64_t pol_c = l2_policy_evict_first();
     uint64_t split_tiles[1];
     uint32_t n_split = 0, sk_seen = 0, local = 0;
-    if (leader) ctl_smem[6] = 0u;  // which of the two pending arrivals were issued
     Cursor cur;
     cursor_init(cur, s, x);
     Item it;
@@ -1021,16 +1045,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           st_release_gpu(p.flags + slot, epoch);
-          // Arrival ticket of the split tile (indexed by its first contributor x0): the
-          // deadlock-free fallback of phase 2 (a reducer that gives up waiting leaves its band
-          // to the tile's last arriver).  Issued after the flag release (acq_rel: ordered
-          // after it), not waited on here.
-          const uint64_t uu = it.tile - s.dp_tiles;
-          const uint64_t x0u = (uu * s.ipt) / s.ipw;
-          const uint32_t old = atom_add_acq_rel_gpu(p.tickets + (epoch & 1u) * kMaxCtas + x0u * CG + rank, 1u);
-          if (sk_seen == 0) pend_old0 = old; else pend_old1 = old;
-          ctl_smem[4 + (sk_seen == 0 ? 0 : 1)] = (uint32_t)uu;
-          ctl_smem[6] |= sk_seen == 0 ? 1u : 2u;
         }
         if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_FLAG);
         // the CTA reduces (phase 2) only the tile of its FIRST Stream-K item
@@ -1112,209 +1126,160 @@ __global__ void __launch_bounds__(kThreads, 1)
   // when the owner x0 has published by the time the peers have (every
   // contributor ends its mainloop together); otherwise the peers are summed
   // first and x0 — whose item may be its LAST — is added when it lands.
+  //
+  // Liveness without co-residency.  Phase 1 never waits on another CTA, so once every
+  // CTA of the launch has STARTED, every partial will be published and the flag waits
+  // below terminate.  Each CTA counts itself on started[par] at kernel start (hidden
+  // behind the mainloop).  A reducer whose flag wait exceeds p.abandon_cycles reads that
+  // counter: if every CTA has started it simply keeps waiting; otherwise (some CTA is
+  // not resident — another grid holds its SM) it marks its band abandoned and exits,
+  // freeing its SM.  The LAST CTA to start (it sees every abandonment made before it
+  // started, and none can be made after) reduces the abandoned bands at its end.  A race
+  // between a reducer that abandons just as the last CTA starts is settled by one CAS on
+  // the band state (1 abandoned -> 2 claimed by the last starter | 3 taken back).
+  // Normally nothing times out: the cost is one atomic per CTA at kernel start.
   __syncwarp();          // producer / MMA lanes rejoin their warps
   phase2_bar_sync();     // split tiles published by the epilogue
   if (s.sk_tiles) {
     const uint32_t ft = threadIdx.x;
     const uint32_t n_split = nsplit_smem[0];
     const uint32_t epoch = nsplit_smem[3];  // read by the epilogue leader at kernel start
+    const uint32_t par = epoch & 1u;
     constexpr uint32_t V = BN / 4;  // float4 column groups per tile row
-    static_assert(C::RING_BYTES >= (uint32_t)kBM * (V + 1) * 16, "phase-2 band stage");
+    static_assert(C::RING_BYTES >= (uint32_t)kBM * (V + 1) * 16 + 4096, "phase-2 band stage + claim list");
     const float4* wsv = reinterpret_cast<const float4*>(p.ws);
     const uint64_t slot_v = (uint64_t)kBM * V;  // float4 per slot
     volatile uint32_t* peers_seen = nsplit_smem + 2;
-    for (uint32_t si = 0; si < n_split; ++si) {
-      const uint64_t u = split_smem[si];
+    volatile uint32_t* p2w = nsplit_smem + 5;  // [0] a wait timed out, [1] decision, [2] owner ready, [3] claims
+    const uint32_t stage = smem_u32(smem);     // idle operand ring: float4 [row][V+1]
+    // Reduce reducer (xr, rk)'s band of split tile u and store it to C.  `bounded`: flag
+    // waits may time out and hand the band to the last starter (the CTA's own band);
+    // otherwise every CTA has started and the waits are plain.
+    auto reduce_band = [&](uint64_t u, uint64_t xr, uint32_t rk, bool bounded, bool stamps) {
       const uint64_t x0 = (u * s.ipt) / s.ipw;
       const uint64_t x1 = ((u + 1) * s.ipt - 1) / s.ipw;
       const uint32_t nc = (uint32_t)(x1 - x0 + 1);
       const bool aligned = x0 * s.ipw == u * s.ipt;  // x0's range starts at tile u
       const uint64_t r_lo = x0 + (aligned ? 0 : 1);
       const uint32_t nr = (uint32_t)(x1 - r_lo + 1);
-      const uint32_t idx = (uint32_t)(x - r_lo);
+      const uint32_t idx = (uint32_t)(xr - r_lo);
       // ragged problems only (M or N not a multiple of the tile): bound the band by the
       // rows / column chunks the contributors wrote (phase 1 skips the rest)
       uint32_t rows_ok = kBM, Vv = V;
+      uint64_t ttm, ttn;
+      tile_rc<RASTER>(s, p.raster, s.dp_tiles + u, ttm, ttn);
       if (p.ragged) {
-        uint64_t utm, utn;
-        tile_rc<RASTER>(s, p.raster, s.dp_tiles + u, utm, utn);
-        const uint64_t tile_rows0 = utm * TILE_M + rank * kBM;
+        const uint64_t tile_rows0 = ttm * TILE_M + rk * kBM;
         if (tile_rows0 >= p.M)
           rows_ok = 0;  // this row half of the tile is entirely past M: empty band below
         else if (p.M - tile_rows0 < (uint64_t)kBM)
           rows_ok = (uint32_t)(p.M - tile_rows0);  // exact: phase 1 wrote rows < M only
-        const uint64_t tile_cols0 = utn * BN;
+        const uint64_t tile_cols0 = ttn * BN;
         if (p.N - tile_cols0 < (uint64_t)BN) Vv = (uint32_t)((p.N - tile_cols0 + 31) / 32 * 32 / 4);
       }
       const uint32_t R0 = (uint32_t)(((uint64_t)idx * rows_ok) / nr);
       const uint32_t R1 = (uint32_t)(((uint64_t)(idx + 1) * rows_ok) / nr);
-      if (R0 == R1) continue;
+      if (R0 == R1) return;
       // contributor x0+t wrote its first Stream-K item (slot 2*cta), except x0
       // when its range starts inside an earlier tile (tile u is its last item)
-      const uint64_t slot0 = 2 * (x0 * CG + rank) + (aligned ? 0 : 1);
-      const uint64_t tile = s.dp_tiles + u;
-      uint64_t ttm, ttn;
-      tile_rc<RASTER>(s, p.raster, tile, ttm, ttn);
-      const uint64_t row0 = ttm * TILE_M + rank * kBM + R0;
+      const uint64_t slot0 = 2 * (x0 * CG + rk) + (aligned ? 0 : 1);
+      const uint64_t row0 = ttm * TILE_M + rk * kBM + R0;
       const uint64_t gcol0 = ttn * BN;
-      const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc,
-                          p.timeline ? p.timeline + (uint64_t)blockIdx.x * TL_EVENTS : nullptr};
-      const uint32_t stage = smem_u32(smem);  // idle operand ring: float4 [row][V+1]
+      const ReduceArgs ra{wsv, slot_v, slot0, x0, rk, nc,
+                          (p.timeline && stamps) ? p.timeline + (uint64_t)blockIdx.x * TL_EVENTS : nullptr};
+      uint32_t* bst = p.bstate + par * kMaxCtas + xr * CG + rk;
       // Peer flags are awaited by one thread each; thread kThreads-1 polls the
-      // owner's flag until either it is up or every peer has been seen.  Every wait is
-      // bounded by p.abandon_cycles: a contributor that has not published by then may not
-      // be resident (another grid holding SMs), so this reducer hands its band to the
-      // tile's last arriver instead of spinning (abandon protocol below).
-      if (ft == 0) {
-        *peers_seen = 0u;
-        ctl_smem[1] = 0u;  // abandon requested
-      }
-      phase2_bar_sync();
-      const long long wait_t0 = clock64();
-      if (ft < kThreads - 1) {
-        for (uint32_t t = 1 + ft; t < nc; t += kThreads - 1) {
-          if (!wait_flag_until(p.flags + 2 * ((x0 + t) * CG + rank), epoch, wait_t0, p.abandon_cycles)) {
-            ctl_smem[1] = 1u;
-            break;
-          }
-          atomicAdd(const_cast<uint32_t*>(peers_seen), 1u);
-        }
-      }
-      if (ft == kThreads - 1) {
-        const uint32_t want = nc - 1;
-        uint32_t ready = 0;
-        while (true) {
-          if (ld_acquire_gpu(p.flags + slot0) == epoch) { ready = 1; break; }
-          if (*peers_seen >= want) break;
-          if (*reinterpret_cast<volatile uint32_t*>(ctl_smem + 1) != 0u ||
-              clock64() - wait_t0 > (long long)p.abandon_cycles) {
-            ctl_smem[1] = 1u;
-            break;
-          }
-        }
-        ctl_smem[7] = ready;
-      }
-      phase2_bar_sync();
-      bool owner_ready = ctl_smem[7] != 0 && !(p.debug & 1u);
-      if (ctl_smem[1] != 0u) {
-        // Abandon protocol (thread 0): mark the band abandoned, then register on the tile's
-        // ticket.  If every contributor has arrived by then, take the band back and reduce
-        // it now (exactly one of this CAS and the last arriver's claim succeeds); otherwise
-        // the last arriver — which sees this abandonment on the ticket — reduces it.
+      // owner's flag until either it is up or every peer has been seen.
+      uint32_t limit = bounded ? p.abandon_cycles : 0xFFFFFFFFu;
+      while (true) {
         if (ft == 0) {
-          uint32_t* st = p.bstate + (epoch & 1u) * kMaxCtas + (x * CG + rank);
-          atom_cas_acq_rel_gpu(st, 0u, 1u);
-          const uint32_t tk = atom_add_acq_rel_gpu(p.tickets + (epoch & 1u) * kMaxCtas + x0 * CG + rank, 1u << 16);
-          uint32_t mine = 0;
-          if ((tk & 0xFFFFu) == nc && atom_cas_acq_rel_gpu(st, 1u, 3u) == 1u) mine = 1;
-          ctl_smem[1] = mine ? 2u : 3u;
+          *peers_seen = 0u;
+          p2w[0] = 0u;
         }
         phase2_bar_sync();
-        if (ctl_smem[1] == 3u) {
-          phase2_bar_sync();  // ctl_smem[1] is rewritten by the next split tile
-          continue;           // the last arriver reduces this band
+        const long long t0 = clock64();
+        if (ft < kThreads - 1) {
+          for (uint32_t t = 1 + ft; t < nc; t += kThreads - 1) {
+            if (!wait_flag_until(p.flags + 2 * ((x0 + t) * CG + rk), epoch, t0, limit)) {
+              atomicOr(const_cast<uint32_t*>(p2w), 1u);  // read by the owner poller meanwhile
+              break;
+            }
+            atomicAdd(const_cast<uint32_t*>(peers_seen), 1u);
+          }
         }
-        owner_ready = !(p.debug & 1u);  // every contributor has published
+        if (ft == kThreads - 1) {
+          const uint32_t want = nc - 1;
+          uint32_t ready = 0;
+          while (true) {
+            if (ld_acquire_gpu(p.flags + slot0) == epoch) { ready = 1; break; }
+            if (*peers_seen >= want || p2w[0] != 0u) break;
+            if (clock64() - t0 > (long long)limit) {
+              atomicOr(const_cast<uint32_t*>(p2w), 1u);
+              break;
+            }
+          }
+          p2w[2] = ready;
+        }
+        phase2_bar_sync();
+        if (p2w[0] == 0u) break;
+        // a wait timed out: keep waiting if every CTA has started, else hand the band off
+        if (ft == 0) p2w[1] = limit == 0xFFFFFFFFu ? 1u : abandon_or_wait(p.hdr, par, bst);
+        phase2_bar_sync();
+        if (p2w[1] == 0u) {
+          phase2_bar_sync();  // p2w is rewritten by the next band
+          return;             // the last CTA to start reduces this band
+        }
+        limit = 0xFFFFFFFFu;
       }
-      if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_WAITED);
+      if (stamps) SKPP_STAMP(p, TL_WAITED);
+      const bool owner_ready = p2w[2] != 0u && !(p.debug & 1u);
       const uint32_t nrows = R1 - R0;
       band_reduce<CG, V>(ra, R0, nrows, Vv, 0, owner_ready ? nc : nc - 1, false, stage, ft);
-      if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM1);
+      if (stamps) SKPP_STAMP(p, TL_SUM1);
       if (!owner_ready) {
-        // the owner's flag (every peer has published); bounded like the waits above
         if (ft == 0) {
-          uint32_t ok = wait_flag_until(p.flags + slot0, epoch, clock64(), p.abandon_cycles) ? 1u : 0u;
-          if (!ok) {
-            uint32_t* st = p.bstate + (epoch & 1u) * kMaxCtas + (x * CG + rank);
-            atom_cas_acq_rel_gpu(st, 0u, 1u);
-            const uint32_t tk = atom_add_acq_rel_gpu(p.tickets + (epoch & 1u) * kMaxCtas + x0 * CG + rank, 1u << 16);
-            ok = ((tk & 0xFFFFu) == nc && atom_cas_acq_rel_gpu(st, 1u, 3u) == 1u) ? 1u : 0u;
+          uint32_t go = 1u;
+          if (!wait_flag_until(p.flags + slot0, epoch, clock64(), limit)) {
+            go = abandon_or_wait(p.hdr, par, bst);
+            if (go) wait_flag(p.flags + slot0, epoch);
           }
-          ctl_smem[1] = ok;
+          p2w[1] = go;
         }
         phase2_bar_sync();  // also orders the stage writes above before the re-reads below
-        if (ctl_smem[1] == 0u) {
+        if (p2w[1] == 0u) {
           phase2_bar_sync();
-          continue;  // handed to the last arriver
+          return;  // handed to the last starter (the peers' partial sums are discarded)
         }
         band_reduce<CG, V>(ra, R0, nrows, Vv, nc - 1, nc, true, stage, ft);
-        if (ft == kEpiWarp0 * 32 && si == 0) SKPP_STAMP(p, TL_SUM2);
+        if (stamps) SKPP_STAMP(p, TL_SUM2);
       }
       phase2_bar_sync();
       band_store<V>(p, stage, nrows, Vv, row0, gcol0, ft);
-      phase2_bar_sync();  // stage and nsplit_smem[1..2] are reused by the next split tile
-    }
-    // ---- last arriver: reduce the bands whose reducers gave up before the tile's last
-    // arrival.  The leader's ticket arrivals (phase 1) returned (abandons << 16 | earlier
-    // arrivals); the arrival that completed a tile (earlier arrivals + 1 == nc) with
-    // abandons > 0 claims every band still marked abandoned (CAS 1 -> 2; a reducer that
-    // abandoned after this arrival saw the full count and took its band back, CAS 1 -> 3).
-    // Normally nothing is abandoned: one barrier, no memory traffic.
-    if (ft == kEpiWarp0 * 32) {
-      uint32_t todo = 0;
-      const uint32_t valid = ctl_smem[6];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        if (!(valid >> j & 1u)) continue;
-        const uint32_t old = j == 0 ? pend_old0 : pend_old1;
-        const uint64_t u = ctl_smem[4 + j];
-        const uint64_t x0 = (u * s.ipt) / s.ipw, x1 = ((u + 1) * s.ipt - 1) / s.ipw;
-        if ((old & 0xFFFFu) + 1u == (uint32_t)(x1 - x0 + 1) && (old >> 16) != 0u) todo |= 1u << j;
-      }
-      ctl_smem[8] = todo;
-    }
-    phase2_bar_sync();
-    const uint32_t todo = ctl_smem[8];
-    for (int j = 0; j < 2; ++j) {
-      if (!(todo >> j & 1u)) continue;
-      const uint64_t u = ctl_smem[4 + j];
-      const uint64_t x0 = (u * s.ipt) / s.ipw, x1 = ((u + 1) * s.ipt - 1) / s.ipw;
-      const uint32_t nc = (uint32_t)(x1 - x0 + 1);
-      const bool aligned = x0 * s.ipw == u * s.ipt;
-      const uint64_t r_lo = x0 + (aligned ? 0 : 1);
-      const uint32_t nr = (uint32_t)(x1 - r_lo + 1);
-      uint32_t* mask = ctl_smem + 9;
-      if (ft < 32) mask[ft] = 0u;
+      phase2_bar_sync();  // stage and p2w are reused by the next band
+    };
+    for (uint32_t si = 0; si < n_split; ++si)
+      reduce_band(split_smem[si], x, rank, true, ft == kEpiWarp0 * 32 && si == 0);
+    // The last CTA to start: reduce every band abandoned in this launch.
+    if (nsplit_smem[4] != 0u) {
+      uint32_t* list = reinterpret_cast<uint32_t*>(smem + C::RING_BYTES - 4096);
+      if (ft == 0) p2w[3] = 0u;
       phase2_bar_sync();
-      for (uint32_t i = ft; i < nr; i += kThreads) {
-        uint32_t* st = p.bstate + (epoch & 1u) * kMaxCtas + (r_lo + i) * CG + rank;
-        if (ld_acquire_gpu(st) == 1u && atom_cas_acq_rel_gpu(st, 1u, 2u) == 1u) atomicOr(mask + (i >> 5), 1u << (i & 31));
+      for (uint32_t c = ft; c < gridDim.x; c += kThreads) {
+        uint32_t* st = p.bstate + par * kMaxCtas + c;
+        if (ld_acquire_gpu(st) == 1u && atom_cas_acq_rel_gpu(st, 1u, 2u) == 1u)
+          list[atomicAdd(const_cast<uint32_t*>(p2w + 3), 1u)] = c;
       }
       phase2_bar_sync();
-      uint32_t rows_ok = kBM, Vv = V;
-      uint64_t utm, utn;
-      tile_rc<RASTER>(s, p.raster, s.dp_tiles + u, utm, utn);
-      if (p.ragged) {
-        const uint64_t tile_rows0 = utm * TILE_M + rank * kBM;
-        rows_ok = tile_rows0 >= p.M ? 0u : (p.M - tile_rows0 < (uint64_t)kBM ? (uint32_t)(p.M - tile_rows0) : kBM);
-        const uint64_t tile_cols0 = utn * BN;
-        if (p.N - tile_cols0 < (uint64_t)BN) Vv = (uint32_t)((p.N - tile_cols0 + 31) / 32 * 32 / 4);
-      }
-      const uint64_t slot0 = 2 * (x0 * CG + rank) + (aligned ? 0 : 1);
-      const ReduceArgs ra{wsv, slot_v, slot0, x0, rank, nc, nullptr};
-      const uint32_t stage = smem_u32(smem);
-      for (uint32_t idx = 0; idx < nr; ++idx) {
-        if (!(mask[idx >> 5] >> (idx & 31) & 1u)) continue;
-        const uint32_t R0 = (uint32_t)(((uint64_t)idx * rows_ok) / nr);
-        const uint32_t R1 = (uint32_t)(((uint64_t)(idx + 1) * rows_ok) / nr);
-        if (R0 == R1) continue;
-        band_reduce<CG, V>(ra, R0, R1 - R0, Vv, 0, nc, false, stage, ft);
-        phase2_bar_sync();
-        band_store<V>(p, stage, R1 - R0, Vv, utm * TILE_M + rank * kBM + R0, utn * BN, ft);
-        phase2_bar_sync();
-      }
-    }
-    // Zero the other parity's tickets and band states for the next Stream-K launch on
-    // this workspace (it starts touching them only after this grid has completed).
-    if (ft < 32) {
-      const uint32_t np = (epoch & 1u) ^ 1u;
-      for (uint32_t i = blockIdx.x + gridDim.x * ft; i < kMaxCtas; i += 32 * gridDim.x) {
-        p.tickets[np * kMaxCtas + i] = 0u;
-        p.bstate[np * kMaxCtas + i] = 0u;
+      const uint32_t n_claimed = p2w[3];
+      for (uint32_t i = 0; i < n_claimed; ++i) {
+        const uint32_t c = list[i];
+        const uint64_t xr = c / CG;
+        reduce_band((xr * s.ipw) / s.ipt, xr, c % CG, false, false);
       }
     }
     if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
   }
+  if (threadIdx.x == 0) SKPP_STAMP(p, TL_END);
 
   tc_fence_before();
   if constexpr (CG == 2) {
@@ -1727,9 +1692,11 @@ extern "C" int skpp_plan_create(const skpp_problem_t* p, const skpp_tile_t* t,
       delete pl;
       return rc;
     }
-    if ((int64_t)g > co) {
+    // Persistent grid: one wave of workgroups.  (Liveness does not depend on it — see the
+    // phase-2 protocol — but a grid of several waves would serialise its fixups.)
+    if ((int64_t)g > co || (uint64_t)g * (t->blk_m > (uint32_t)kBM ? 2 : 1) > kMaxCtas) {
       set_error("g=" + std::to_string(g) + " exceeds the " + std::to_string(co) +
-                " co-resident CTAs the Stream-K fixup needs");
+                " co-resident workgroups of a persistent Stream-K grid");
       delete pl;
       return SKPP_EGRID;
     }
@@ -1882,7 +1849,6 @@ extern "C" int skpp_plan_launch(void* plan, void* workspace, uint64_t workspace_
       uint8_t* base = reinterpret_cast<uint8_t*>(workspace);
       gp.hdr = reinterpret_cast<uint32_t*>(base);
       gp.flags = reinterpret_cast<uint32_t*>(base + kWsFlagsOff);
-      gp.tickets = reinterpret_cast<uint32_t*>(base + kWsTicketsOff);
       gp.bstate = reinterpret_cast<uint32_t*>(base + kWsStatesOff);
       gp.ws = reinterpret_cast<float*>(base + kWsCtlBytes);
       pl->ws_bound = workspace;

@@ -1,11 +1,12 @@
 """Liveness of Stream-K grids that share the GPU (run on a B200 via gpurun).
 
-Phase-2 reducers wait for peer flags at most ~20 us; a reducer that gives up marks its band
-abandoned and the tile's last arriving contributor reduces it (or the reducer takes it back
-when everyone has arrived meanwhile), so no CTA ever waits on a CTA that is not resident.
+Phase-2 reducers wait for peer flags at most ~20 us; then, if some CTA of the launch has not
+started yet (its SM is held by another grid), the reducer marks its band abandoned and exits,
+and the last CTA to start reduces it; if every CTA has started, waiting is safe and it keeps
+waiting.  So no CTA ever waits on a CTA that is not resident.
 These tests drive that: concurrent Stream-K grids on prioritised streams, two processes on
-one GPU, a GEMM that runs while 100 of the 148 SMs are held by another grid, and the
-abandon path forced on every band (skpp_set_debug bit 1) — all bitwise.
+one GPU, a GEMM that runs while 140 (or 100) of the 148 SMs are held by another grid, and a
+zero wait bound on every phase-2 wait (skpp_set_debug bit 1) — all bitwise.
 """
 
 import os
@@ -49,7 +50,15 @@ def test_two_processes_share_one_gpu():
 
 
 def test_gemm_completes_while_partially_resident():
-    (rc, out), = _run_workers([("partial", 3, 100, 14)], timeout=180)
+    """With 140 of 148 SMs held, the 148-CTA grid runs 8 CTAs at a time: reducers time out while
+    CTAs have not started, abandon their bands, and the last CTA to start reduces them — the
+    path must actually be taken (abandoned bands are counted in the workspace header).  With
+    100 SMs held (the CTA-pair tile included) the grid also completes, bitwise."""
+    (rc, out), = _run_workers([("partial", 2, 140, 14)], timeout=180)
+    assert rc == 0 and out.strip().endswith("ok"), out[-2000:]
+    total = int(out.split("abandoned_total=")[1].split()[0])
+    assert total > 0, out[-2000:]
+    (rc, out), = _run_workers([("partial", 3, 100, 15)], timeout=180)
     assert rc == 0 and out.strip().endswith("ok"), out[-2000:]
 
 
@@ -57,9 +66,9 @@ def test_gemm_completes_while_partially_resident():
 @pytest.mark.parametrize("tile,shape", [((128, 128, 64), (512, 512, 8192)), ((128, 128, 128), (16, 4096, 4096)),
                                         ((256, 256, 128), (600, 392, 4096)), ((128, 64, 128), (1, 4096, 65536))])
 def test_abandon_path_bit_identical(debug, tile, shape):
-    """Bound 0 on every phase-2 wait: bands not already published are abandoned and reduced by
-    the last arriver (or reclaimed); every policy stays bitwise on integer inputs and bit-identical
-    to the normal path on randn inputs."""
+    """Bound 0 on every phase-2 wait: every wait that is not already satisfied goes through the
+    timeout decision (keep waiting when every CTA has started, else abandon to the last starter);
+    every policy stays bitwise on integer inputs and bit-identical to the normal path on randn."""
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import _lib
     from oracle import gemm as ogemm

@@ -46,6 +46,8 @@ def main() -> None:
 
     from paper_2408_11417_b200 import _lib
 
+    if os.environ.get("SKPP_DEBUG"):
+        _lib.lib.skpp_set_debug(int(os.environ["SKPP_DEBUG"]))
     if os.environ.get("SKPP_L2_HINTS"):
         _lib.lib.skpp_set_l2_hints(int(os.environ["SKPP_L2_HINTS"]))
 

@@ -9,7 +9,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-EVENTS = ["start", "first_tma", "first_full", "mma_done", "phase1", "waited", "phase2", "-", "epi_first", "part_issued", "part_flag", "sum1", "sum2"]
+EVENTS = ["start", "first_tma", "first_full", "mma_done", "phase1", "waited", "phase2", "end", "epi_first", "part_issued", "part_flag", "sum1", "sum2"]
 
 
 def main() -> None:
