@@ -328,25 +328,43 @@ def roofline(flops: float, nbytes: float, seconds: float, peaks: dict, sustained
             "peak_source": peaks["source"] + ", copy bandwidth"}
 
 
-def fixup_summary(plan, tile, flops: float, nbytes: float, seconds: float) -> dict:
-    """Stream-K partial-tile traffic of one launch (reported beside the roofline).
+def fixup_summary(plan, tile, policy, workload: str, flops: float, nbytes: float, seconds: float) -> dict:
+    """Stream-K partial-tile (fixup workspace) traffic of one launch.
 
-    Every partial item (owner and peers) writes its 128 x blk_n fp32 accumulator per CTA row
-    half once and the reducers read it back once, so bytes = 2 x items x blk_m x blk_n x 4 —
-    an upper bound when the last row / column tile is ragged (valid chunks only)."""
+    Analytic: every partial item writes its valid rows x columns of fp32 once and the reducers
+    read them back once.  Measured: the committed ncu difference between this shape's Stream-K
+    launch and its data-parallel launch (same operands, same C): L2 write sectors and DRAM bytes
+    (profiles/round2/ncu_fixup.json, tools/fixup_traffic.py), when that capture is of this
+    (tile, policy)."""
     from paper_2408_11417_b200.scheduler import count_partials
+    from paper_2408_11417_b200.tiles import tile_label
 
     partial, full, peers = count_partials(plan.sched_c)
-    per_item = tile.blk_m * tile.blk_n * 4
+    per_item = min(tile.blk_m, plan.size.m) * min(tile.blk_n, plan.size.n) * 4
     written = partial * per_item
-    return {
+    out = {
         "partial_items": partial, "non_owner_partials": peers, "full_tile_stores": full,
-        "bytes_written": written, "bytes_read": written,
+        "analytic_bytes_written": written, "analytic_bytes_read": written,
         "vs_algorithmic_bytes": round(2 * written / nbytes, 3),
-        "avg_rate_over_step_gbs": round(2 * written / seconds / 1e9, 1),
-        "note": "partials live in L2 within a launch (ncu DRAM bytes ~= algorithmic); their cost is "
-                "the SM store port (<= 60 GB/s per SM) and the ~7 TB/s chip L2 write rate",
+        "analytic_rate_over_step_gbs": round(2 * written / seconds / 1e9, 1),
+        "measured": None,
     }
+    try:
+        with open(os.path.join(ROOT, "profiles", "round2", "ncu_fixup.json")) as fh:
+            rows = json.load(fh)["rows"]
+        row = next(r for r in rows if r["workload"] == workload and r["tile"] == tile_label(tile)
+                   and policy.label == "hybrid1")
+        out["measured"] = {k: row[k] for k in ("workspace_dram_bytes", "workspace_hbm_gbs", "workspace_hbm_frac_of_peak",
+                                               "l2_write_bytes_delta", "l2_write_delta_vs_analytic",
+                                               "dp_l2_write_bytes_vs_c_bytes", "workspace_l2_write_gbs",
+                                               "sk_duration_us", "source")}
+        out["measured"]["file"] = "profiles/round2/ncu_fixup.json"
+        out["measured"]["note"] = ("ncu (Stream-K launch) - (data-parallel launch): the partials stay in L2 "
+                                   "(workspace HBM traffic ~0); L2 write sectors count 1.5x the stored bytes on "
+                                   "this part for C as well (dp_l2_write_bytes_vs_c_bytes)")
+    except (OSError, ValueError, KeyError, StopIteration):
+        pass
+    return out
 
 
 def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool, max_seconds: float,
@@ -630,7 +648,7 @@ def run_ours(args, wl: dict) -> None:
                 "note": "per-(tile, policy) times from CUDA-graph replays with warm L2 (selection sweep)",
             },
             "roofline": roof,
-            "fixup": fixup_summary(plan, tile, flops, nbytes, per_step_s),
+            "fixup": fixup_summary(plan, tile, policy, args.workload, flops, nbytes, per_step_s),
             "sweep": sweep_block,
             "cpu_baseline": {
                 "value": round(cpu_value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
