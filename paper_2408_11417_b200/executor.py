@@ -286,6 +286,16 @@ class GemmPlan:
             handle = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(self.device)
             self._private_ws = _new_workspace(self.ws_bytes, self.device, handle)
 
+    def share_workspace_of(self, other: "GemmPlan") -> None:
+        """Capture this plan's launches on ``other``'s private workspace.  Only for launches
+        that run strictly one after another (e.g. a rotation of plans inside one graph)."""
+        if not self.ws_bytes:
+            return
+        other.prepare_for_capture()
+        if other._private_ws is None or other._private_ws.numel() < self.ws_bytes:
+            raise ValueError("the other plan's workspace is too small for this plan")
+        self._private_ws = other._private_ws
+
     def launch(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         handle = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(self.device)
         if self.ws_bytes and _is_capturing(handle):

@@ -51,6 +51,14 @@ class MeasureParams:
     peak_tflops: float = DENSE_BF16_PEAK_TFLOPS
     use_graphs: bool = True
     timed_us: float = 20000.0  # timed work per schedule for big problems (>= 3 samples)
+    # Cold L2: sizes whose operand set (A, B, C) is at least cold_min_bytes and fits in the
+    # L2 are timed rotating over enough distinct operand sets (> 4 x L2 in total, at most
+    # cold_max_sets) that every launch reads its operands from HBM, as in production and in
+    # bench.py's timed region.  Warm timing picked a different winner for 16 of 628 such
+    # sizes, 4 of them > 20% slower cold (profiles/round2/cold_l2_check.json).
+    cold: bool = False
+    cold_min_bytes: int = 4 << 20
+    cold_max_sets: int = 64
 
 
 class OperandPool:
@@ -92,8 +100,51 @@ def _side_stream(device: int) -> torch.cuda.Stream:
     return st
 
 
-def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None) -> float:
-    """Median per-launch device time (microseconds) of a prepared GEMM."""
+L2_BYTES = 126 * 1024 * 1024
+
+
+def cold_sets(size: ProblemSize, params: MeasureParams) -> int:
+    """Operand sets a cold measurement of ``size`` rotates over (0 = time it warm)."""
+    b = 2 * (size.m * _pad8(size.k) + _pad8(size.k) * _pad8(size.n)) + 4 * size.m * _pad8(size.n)
+    if not params.cold or b < params.cold_min_bytes or b > L2_BYTES:
+        return 0
+    return int(min(params.cold_max_sets, max(2, math.ceil(4 * L2_BYTES / b))))
+
+
+class ColdPool:
+    """Raw device memory carved into rotating operand sets for cold-L2 timing."""
+
+    def __init__(self, params: MeasureParams, device: int | None = None, seed: int = 0):
+        dev = torch.cuda.current_device() if device is None else device
+        # n sets of b bytes with n = ceil(4 L2 / b) <= 5 for b <= L2 (and n * b <= 64 x b for small b)
+        self.nbytes = 5 * L2_BYTES + (64 << 20)
+        gen = torch.Generator(device=f"cuda:{dev}")
+        gen.manual_seed(seed)
+        self.raw = torch.randn(self.nbytes // 2, generator=gen, device=f"cuda:{dev}").to(params.in_dtype)
+        self.out_dtype = params.out_dtype
+
+    def sets(self, size: ProblemSize, n: int):
+        kp, np_ = _pad8(size.k), _pad8(size.n)
+        ea, eb = size.m * kp, kp * np_
+        ec = size.m * np_ * (4 if self.out_dtype == torch.float32 else 2) // 2  # in 16-bit elements
+        step = (ea + eb + ec + 63) // 64 * 64
+        if n * step > self.raw.numel():
+            raise ValueError("cold pool too small")
+        out = []
+        for r in range(n):
+            base = self.raw[r * step:(r + 1) * step]
+            a = base[:ea].view(size.m, kp)[:, : size.k]
+            b = base[ea:ea + eb].view(kp, np_)[: size.k, : size.n]
+            c = base[ea + eb:ea + eb + ec].view(torch.uint8).view(self.out_dtype).view(size.m, np_)[:, : size.n]
+            out.append((a, b, c))
+        return out
+
+
+def time_plan(plan, params: MeasureParams, est_us: float | None = None) -> float:
+    """Median per-launch device time (microseconds) of a prepared GEMM, or of a rotation of
+    prepared GEMMs over distinct operand sets (a list of plans: cold L2)."""
+    if isinstance(plan, (list, tuple)):
+        return _time_rotation(list(plan), params)
     stream = torch.cuda.current_stream()
     if params.warmup:
         plan.launch()
@@ -154,6 +205,40 @@ def time_plan(plan: GemmPlan, params: MeasureParams, est_us: float | None = None
     return times[len(times) // 2]
 
 
+def _time_rotation(plans: list, params: MeasureParams) -> float:
+    """Cold timing: one graph launches every plan of the rotation once (each on its own
+    operand set, all on one shared workspace); median per-launch time over replays."""
+    stream = torch.cuda.current_stream()
+    side = _side_stream(stream.device_index)
+    plans[0].prepare_for_capture(side)
+    for p in plans[1:]:
+        p.share_workspace_of(plans[0])
+    side.wait_stream(stream)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        for p in plans[: params.warmup]:
+            p.launch()
+        graph.capture_begin()
+        try:
+            for p in plans:
+                p.launch()
+        finally:
+            graph.capture_end()
+    stream.wait_stream(side)
+    graph.replay()
+    events = []
+    for _ in range(max(3, min(params.reps, 5))):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        graph.replay()
+        e1.record(stream)
+        events.append((e0, e1))
+    events[-1][1].synchronize()
+    times = sorted(e0.elapsed_time(e1) * 1e3 / len(plans) for e0, e1 in events)
+    return times[len(times) // 2]
+
+
 def measure_size(
     size: ProblemSize,
     tile: TileShape,
@@ -161,8 +246,12 @@ def measure_size(
     policies: list[Policy],
     params: MeasureParams,
     pool: OperandPool,
+    cold_pool: "ColdPool | None" = None,
 ) -> TuneRecord:
     """Time every policy's schedule for one size (identical schedules measured once).
+
+    With ``params.cold`` (and a ``cold_pool``), sizes whose operands fit in the L2 are timed
+    cold: each schedule rotates over :func:`cold_sets` distinct operand sets.
 
     Heavy sizes (a first launch >= ``HEAVY_US``) run at the power cap, where the clock
     needs tens of milliseconds to settle after the load changes: measured in one pass,
@@ -182,6 +271,12 @@ def measure_size(
         plans.setdefault(sig, plan)
         sig_of.append((pol, sig))
     order = list(plans)
+    n_cold = cold_sets(size, params) if cold_pool is not None else 0
+    if n_cold:
+        sets = cold_pool.sets(size, n_cold)
+        times = {sig: time_plan([GemmPlan(sa, sb, sc, plans[sig].policy, tile, g) for sa, sb, sc in sets], params)
+                 for sig in order}
+        return _record(size, params, plans, sig_of, times)
     first = plans[order[0]]
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -208,6 +303,10 @@ def measure_size(
     else:
         for sig in order:
             times[sig] = time_plan(plans[sig], params, first_us if sig == order[0] else None)
+    return _record(size, params, plans, sig_of, times)
+
+
+def _record(size, params, plans, sig_of, times) -> TuneRecord:
     by_sig: dict[tuple, CostEstimate] = {}
     costs = []
     for pol, sig in sig_of:
@@ -293,15 +392,29 @@ def tune_sizes(
         g = default_g(tile)
     if pool is None:
         pool = OperandPool(sizes, params.in_dtype, params.out_dtype)
+    cold_pool = None
+    if params.cold and any(cold_sets(z, params) for z in sizes):
+        cold_pool = _cold_pool(params)
     out = []
     for i, size in enumerate(sizes):
         t0 = time.perf_counter() if seconds is not None else 0.0
-        out.append(measure_size(size, tile, g, policies, params, pool))
+        out.append(measure_size(size, tile, g, policies, params, pool, cold_pool))
         if seconds is not None:
             seconds[size] = seconds.get(size, 0.0) + time.perf_counter() - t0
         if progress is not None:
             progress(i + 1, len(sizes))
     return out
+
+
+_COLD_POOLS: dict = {}
+
+
+def _cold_pool(params: MeasureParams) -> ColdPool:
+    """One cold pool per (device, dtypes), reused by every tile of a sweep."""
+    key = (torch.cuda.current_device(), params.in_dtype, params.out_dtype, params.cold_max_sets)
+    if key not in _COLD_POOLS:
+        _COLD_POOLS[key] = ColdPool(params)
+    return _COLD_POOLS[key]
 
 
 def estimated_cost_s(size: ProblemSize, n_policies: int = 7, peak_tflops: float = 1000.0,
@@ -517,6 +630,9 @@ def main(argv=None) -> int:
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--max-gflop", type=float, default=0.0, help="skip sizes above this (0 = no limit)")
+    ap.add_argument("--cold", action="store_true",
+                    help="time sizes whose operands fit in the L2 cold (rotating operand sets), as production "
+                         "and bench.py see them")
     ap.add_argument("--validate", action="store_true", help="re-measure everything (held-out run)")
     ap.add_argument("--heldout", type=int, default=0, help="also measure N off-grid sizes")
     ap.add_argument("--cost-table", default="",
@@ -538,7 +654,7 @@ def main(argv=None) -> int:
     if args.max_gflop > 0:
         sizes = [s for s in sizes if s.flops <= args.max_gflop * 1e9]
     tiles = [parse_tile(t) for t in args.tiles.split(",")]
-    params = MeasureParams(warmup=args.warmup, reps=args.reps)
+    params = MeasureParams(warmup=args.warmup, reps=args.reps, cold=args.cold)
     dist = None
     if world > 1:
         import torch.distributed as dist

@@ -336,3 +336,29 @@ def test_concurrent_streams_each_with_its_own_workspace():
     torch.cuda.synchronize()
     for p, want in zip(plans, wants):
         assert np.array_equal(p.c.double().cpu().numpy(), want)
+
+
+def test_sweep_cold_timing_rotates_operand_sets():
+    """MeasureParams(cold=True): sizes whose operands fit in L2 are timed rotating over
+    distinct operand sets (> 4 x L2 in total); the record is a normal ranked TuneRecord, and a
+    rotated plan computes the same product as the pool's plan (views carved from the cold pool)."""
+    import paper_2408_11417_b200 as m
+    from paper_2408_11417_b200 import sweep
+
+    size = m.ProblemSize(512, 2048, 2048)
+    params = sweep.MeasureParams(warmup=2, reps=5, cold=True)
+    n = sweep.cold_sets(size, params)
+    assert 2 <= n <= params.cold_max_sets
+    tile = m.TileShape(128, 128, 128)
+    rec, = sweep.tune_sizes([size], tile, None, None, params)
+    assert len(rec.costs) == 7 and all(e.makespan > 0 for _, e in rec.costs)
+    warm, = sweep.tune_sizes([size], tile, None, None, sweep.MeasureParams(warmup=2, reps=5))
+    best = lambda r: min(e.makespan for _, e in r.costs)  # noqa: E731
+    assert best(rec) >= 0.7 * best(warm)  # cold is not (much) faster than warm
+    pool = sweep._cold_pool(params)
+    (a, b, c), = pool.sets(size, 1)
+    a.copy_(torch.randint(-8, 9, a.shape, device="cuda").to(a.dtype))
+    b.copy_(torch.randint(-8, 9, b.shape, device="cuda").to(b.dtype))
+    m.GemmPlan(a, b, c, m.Policy.hybrid(1), tile).launch()
+    torch.cuda.synchronize()
+    assert torch.equal(c.double(), a.double() @ b.double())
