@@ -435,7 +435,12 @@ enum : int {
   TL_BS0 = 13,        // band_sum (first pass, thread 128): clock64 at entry,
   TL_BS1 = 14,        //   after its first batch of partial loads returned,
   TL_BS2 = 15,        //   and at exit (SM cycles, not ns)
-  TL_EVENTS = 16
+  TL_P2_STORED = 16,  // phase 2, thread 0: first band stored to C
+  TL_ENTRY = 21,      // thread 0 at kernel entry (before barrier init and griddepcontrol.wait)
+  TL_C_TMA = 22,      // SM cycles from griddepcontrol.wait returning to the first A load (thread 0)
+  TL_CLK_ENTRY = 24,  // clock64 at TL_ENTRY and at TL_END (thread 0): the SM clock rate over the
+  TL_CLK_END = 31,    //   kernel against %globaltimer
+  TL_EVENTS = 32
 };
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
@@ -719,6 +724,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t x = blockIdx.x / CG;                      // workgroup (pair) id
   const Sched& s = p.s;
 
+  if (threadIdx.x == 0 && p.timeline) {
+    SKPP_STAMP(p, TL_ENTRY);
+    p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CLK_ENTRY] = clock64();
+  }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -758,20 +767,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // While the previous kernel drains, pull the first `p.l2_prefetch` k-blocks of this
-  // workgroup's first item into L2 (A by warp 0, B by warp 3), so the first stages
-  // land from L2 right after the wait below.
-  if ((warp == 0 || warp == 3) && lane == 0 && p.l2_prefetch) {
-    Cursor c0;
-    cursor_init(c0, s, x);
-    Item it0;
-    if (cursor_next(c0, s, x, it0)) {
-      uint64_t tm0, tn0;
-      tile_rc<RASTER>(s, p.raster, it0.tile, tm0, tn0);
-      const int32_t m0 = (int32_t)(tm0 * TILE_M + rank * kBM);
-      const int32_t n0 = (int32_t)(tn0 * BN + rank * C::BNC);
-      const uint64_t kend = it0.kb + p.l2_prefetch < it0.ke ? it0.kb + p.l2_prefetch : it0.ke;
-      for (uint64_t kk = it0.kb; kk < kend; ++kk) {
+  // The producers decode their first item here, before griddepcontrol.wait (it depends only on
+  // the kernel parameters), so the first loads issue right after the wait.  While the previous
+  // kernel drains, they also pull the first `p.l2_prefetch` k-blocks of it into L2 (A by warp 0,
+  // B by warp 3), so the first stages land from L2.
+  Cursor pcur;
+  Item pit;
+  uint64_t ptm = 0, ptn = 0;
+  bool pmore = false;
+  if ((warp == 0 || warp == 3) && lane == 0) {
+    cursor_init(pcur, s, x);
+    pmore = cursor_next(pcur, s, x, pit);
+    if (pmore) tile_rc<RASTER>(s, p.raster, pit.tile, ptm, ptn);
+    if (pmore && p.l2_prefetch) {
+      const int32_t m0 = (int32_t)(ptm * TILE_M + rank * kBM);
+      const int32_t n0 = (int32_t)(ptn * BN + rank * C::BNC);
+      const uint64_t kend = pit.kb + p.l2_prefetch < pit.ke ? pit.kb + p.l2_prefetch : pit.ke;
+      for (uint64_t kk = pit.kb; kk < kend; ++kk) {
         const int32_t k0 = (int32_t)(kk * BK);
         if (warp == 0) {
           if (C::A_OPS > 1 && p.a3d)
@@ -790,6 +802,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // allocation, descriptor and L2 prefetch) overlaps the previous kernel's tail;
   // no global memory written by earlier work is read before this wait.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  const long long c_wait = clock64();
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) SKPP_STAMP(p, TL_START);
 
@@ -803,12 +816,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t stage = 0, phase = 0, kcount = 0, n_full = 0;
     bool first_load = true;
     const uint64_t pol_b = l2_policy_evict_last();
-    Cursor cur;
-    cursor_init(cur, s, x);
-    Item it;
-    while (cursor_next(cur, s, x, it)) {
-      uint64_t tm_, tn_;
-      tile_rc<RASTER>(s, p.raster, it.tile, tm_, tn_);
+    for (; pmore; pmore = cursor_next(pcur, s, x, pit) && (tile_rc<RASTER>(s, p.raster, pit.tile, ptm, ptn), true)) {
+      const Item& it = pit;
+      const uint64_t tm_ = ptm, tn_ = ptn;
       const int32_t m0 = (int32_t)(tm_ * TILE_M + rank * kBM);
       const int32_t n0 = (int32_t)(tn_ * BN + rank * C::BNC);
       // Serpentine K: every other FULL item of this workgroup walks K backwards.  A
@@ -826,6 +836,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++kcount;
           if (first_load) {
             SKPP_STAMP(p, TL_FIRST_TMA);
+            if (p.timeline) p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_C_TMA] = clock64() - c_wait;
             first_load = false;
           }
         }
@@ -1156,8 +1167,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // waits may time out and hand the band to the last starter (the CTA's own band);
     // otherwise every CTA has started and the waits are plain.
     auto reduce_band = [&](uint64_t u, uint64_t xr, uint32_t rk, bool bounded, bool stamps) {
-      const uint64_t x0 = (u * s.ipt) / s.ipw;
-      const uint64_t x1 = ((u + 1) * s.ipt - 1) / s.ipw;
+      const uint64_t x0 = udiv(u * s.ipt, s.ipw);
+      const uint64_t x1 = udiv((u + 1) * s.ipt - 1, s.ipw);
       const uint32_t nc = (uint32_t)(x1 - x0 + 1);
       const bool aligned = x0 * s.ipw == u * s.ipt;  // x0's range starts at tile u
       const uint64_t r_lo = x0 + (aligned ? 0 : 1);
@@ -1177,8 +1188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t tile_cols0 = ttn * BN;
         if (p.N - tile_cols0 < (uint64_t)BN) Vv = (uint32_t)((p.N - tile_cols0 + 31) / 32 * 32 / 4);
       }
-      const uint32_t R0 = (uint32_t)(((uint64_t)idx * rows_ok) / nr);
-      const uint32_t R1 = (uint32_t)(((uint64_t)(idx + 1) * rows_ok) / nr);
+      const uint32_t R0 = (uint32_t)udiv((uint64_t)idx * rows_ok, nr);
+      const uint32_t R1 = (uint32_t)udiv((uint64_t)(idx + 1) * rows_ok, nr);
       if (R0 == R1) return;
       // contributor x0+t wrote its first Stream-K item (slot 2*cta), except x0
       // when its range starts inside an earlier tile (tile u is its last item)
@@ -1255,6 +1266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       phase2_bar_sync();
       band_store<V>(p, stage, nrows, Vv, row0, gcol0, ft);
+      if (bounded && ft == 0) SKPP_STAMP(p, TL_P2_STORED);
       phase2_bar_sync();  // stage and p2w are reused by the next band
     };
     for (uint32_t si = 0; si < n_split; ++si)
@@ -1274,12 +1286,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t i = 0; i < n_claimed; ++i) {
         const uint32_t c = list[i];
         const uint64_t xr = c / CG;
-        reduce_band((xr * s.ipw) / s.ipt, xr, c % CG, false, false);
+        reduce_band(udiv(xr * s.ipw, s.ipt), xr, c % CG, false, false);
       }
     }
     if (ft == kEpiWarp0 * 32) SKPP_STAMP(p, TL_PHASE2);
   }
-  if (threadIdx.x == 0) SKPP_STAMP(p, TL_END);
+  if (threadIdx.x == 0 && p.timeline) {
+    SKPP_STAMP(p, TL_END);
+    p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CLK_END] = clock64();
+  }
 
   tc_fence_before();
   if constexpr (CG == 2) {

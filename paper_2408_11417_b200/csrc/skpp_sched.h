@@ -52,6 +52,18 @@ struct Cursor {
 
 SKPP_HD uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+// a / b.  On the device a 64-bit division is a ~50-instruction subroutine (I2F.U64, MUFU.RCP,
+// F2I.U64 and a correction chain, several hundred cycles of latency); every realistic schedule
+// has its dividends and divisors below 2^32, where the 32-bit sequence is a fraction of that.
+// The producer decodes its first item right after griddepcontrol.wait, so this is on the
+// kernel's critical path.
+SKPP_HD uint64_t udiv(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  if (((a | b) >> 32) == 0) return (uint64_t)((uint32_t)a / (uint32_t)b);
+#endif
+  return a / b;
+}
+
 SKPP_HD void cursor_init(Cursor& c, const Sched& s, uint32_t x) {
   c.part = 0;
   c.sk_cur = min_u64((uint64_t)x * s.ipw, s.sk_iters);
@@ -65,7 +77,7 @@ SKPP_HD bool cursor_next(Cursor& c, const Sched& s, uint32_t x, Item& it) {
     const bool sk_part = (c.part == 0) == (s.sk_first != 0);
     if (sk_part) {
       if (c.sk_cur < c.sk_hi) {
-        const uint64_t u = c.sk_cur / s.ipt;
+        const uint64_t u = udiv(c.sk_cur, s.ipt);
         const uint64_t tile_end = (u + 1) * s.ipt;
         const uint64_t e = min_u64(c.sk_hi, tile_end);
         it.tile = s.dp_tiles + u;
@@ -77,7 +89,7 @@ SKPP_HD bool cursor_next(Cursor& c, const Sched& s, uint32_t x, Item& it) {
           it.role = ROLE_FULL;
         } else if (it.kb == 0) {
           it.role = ROLE_OWNER;
-          it.peer_hi = (tile_end - 1) / s.ipw;
+          it.peer_hi = udiv(tile_end - 1, s.ipw);
         } else {
           it.role = ROLE_PEER;
         }
@@ -102,10 +114,10 @@ SKPP_HD bool cursor_next(Cursor& c, const Sched& s, uint32_t x, Item& it) {
 // Item count of workgroup x without walking the Stream-K part item by item.
 SKPP_HD uint64_t items_of(const Sched& s, uint32_t x) {
   uint64_t n = 0;
-  if (s.dp_tiles > x) n += (s.dp_tiles - x + s.g - 1) / s.g;
+  if (s.dp_tiles > x) n += udiv(s.dp_tiles - x + s.g - 1, s.g);
   const uint64_t lo = min_u64((uint64_t)x * s.ipw, s.sk_iters);
   const uint64_t hi = min_u64((uint64_t)(x + 1) * s.ipw, s.sk_iters);
-  if (hi > lo) n += (hi - 1) / s.ipt - lo / s.ipt + 1;
+  if (hi > lo) n += udiv(hi - 1, s.ipt) - udiv(lo, s.ipt) + 1;
   return n;
 }
 
@@ -116,16 +128,16 @@ SKPP_HD uint64_t items_of(const Sched& s, uint32_t x) {
 // ~g/G columns, so their A and B blocks stay in L2.  The last band has m_tiles % G rows.
 SKPP_HD void tile_coords(const Sched& s, uint32_t band, uint64_t t, uint64_t& tm, uint64_t& tn) {
   if (band == 0) {
-    tm = t / s.n_tiles;
-    tn = t % s.n_tiles;
+    tm = udiv(t, s.n_tiles);
+    tn = t - tm * s.n_tiles;
     return;
   }
-  const uint64_t m_tiles = (s.dp_tiles + s.sk_tiles) / s.n_tiles;
+  const uint64_t m_tiles = udiv(s.dp_tiles + s.sk_tiles, s.n_tiles);
   const uint64_t band_tiles = (uint64_t)band * s.n_tiles;
-  const uint64_t b = t / band_tiles, r = t - b * band_tiles;
+  const uint64_t b = udiv(t, band_tiles), r = t - b * band_tiles;
   const uint64_t rows = m_tiles - b * band < band ? m_tiles - b * band : band;
-  tm = b * band + r % rows;
-  tn = r / rows;
+  tn = udiv(r, rows);
+  tm = b * band + (r - tn * rows);
 }
 
 }  // namespace skpp

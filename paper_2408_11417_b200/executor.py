@@ -136,21 +136,20 @@ def tile_supported(tile: TileShape) -> bool:
     return bool(_lib.lib.skpp_tile_supported(_lib.tile_c(tile)))
 
 
-WS_ZERO_BYTES = 32768  # the control block: header, flags, tickets and band states (skpp_gemm.cu)
 
 
 def _new_workspace(nbytes: int, device: int, stream_handle: int) -> torch.Tensor:
-    """Allocate a fixup workspace on the launch stream and zero its header + flags there.
+    """Allocate a fixup workspace on the launch stream and zero it there.
 
-    Only the header (epoch, arrival counter) and the slot flags need a defined initial
-    value: a slot is read only after its flag equals the launch's epoch.  Allocating and
-    zeroing on the stream the kernel runs on (not torch's current stream) orders the
-    memset before the first launch and ties the block's lifetime to that stream.
+    The kernel needs the control block (epoch header, slot flags, band states) zeroed
+    (skpp.h: "zero-filled the first time it is used"); the whole buffer is zeroed, once per
+    allocation, so no partial slot ever holds recycled memory.  Allocating and zeroing on the
+    stream the kernel runs on (not torch's current stream) orders the memset before the
+    first launch and ties the block's lifetime to that stream.
     """
     size = max(nbytes, 1 << 20)
     with torch.cuda.stream(torch.cuda.ExternalStream(stream_handle, device=f"cuda:{device}")):
-        buf = torch.empty(size, dtype=torch.uint8, device=f"cuda:{device}")
-        buf[:WS_ZERO_BYTES].zero_()
+        buf = torch.zeros(size, dtype=torch.uint8, device=f"cuda:{device}")
     return buf
 
 

@@ -4,6 +4,9 @@
 interleaved round by round.  Prints one JSON line per shape with the median us per build.
 
     python tools/ab_libs.py --libs tools/ab_libs/libskpp_base.so,paper_2408_11417_b200/libskpp.so
+
+An entry may carry a debug switch of the build: ``path@DEBUG`` calls skpp_set_debug(DEBUG) before
+the plans are made.  SKPP_AB_CASES="m:n:k:tile:policy,..." replaces the default shapes.
 """
 
 from __future__ import annotations
@@ -32,6 +35,10 @@ def worker(cases) -> None:
 
     if hasattr(_lib.lib, "skpp_set_cooperative"):
         _lib.lib.skpp_set_cooperative(0)
+    if os.environ.get("SKPP_DEBUG"):
+        _lib.lib.skpp_set_debug(int(os.environ["SKPP_DEBUG"]))
+    if os.environ.get("SKPP_AB_CASES"):
+        cases = [tuple(int(v) if v.isdigit() else v for v in c.split(":")) for c in os.environ["SKPP_AB_CASES"].split(",")]
     out = {}
     for m, n, k, tl, pol in cases:
         tile, policy = parse_tile(tl), parse_policy(sk, pol)
@@ -71,7 +78,10 @@ def main() -> None:
     per = {lib: [] for lib in libs}
     for _ in range(args.rounds):
         for lib in libs:
-            env = dict(os.environ, SKPP_LIB=os.path.abspath(lib))
+            path, *sw = lib.split("@")
+            env = dict(os.environ, SKPP_LIB=os.path.abspath(path))
+            if sw:
+                env["SKPP_DEBUG"] = sw[0]
             r = subprocess.run([sys.executable, __file__, "--libs", lib, "--worker"], env=env, capture_output=True,
                                text=True, timeout=900)
             line = next((ln for ln in r.stdout.splitlines() if ln.startswith("RESULT ")), None)

@@ -9,7 +9,9 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-EVENTS = ["start", "first_tma", "first_full", "mma_done", "phase1", "waited", "phase2", "end", "epi_first", "part_issued", "part_flag", "sum1", "sum2"]
+EVENTS = ["start", "first_tma", "first_full", "mma_done", "phase1", "waited", "phase2", "end", "epi_first", "part_issued", "part_flag", "sum1", "sum2", "-", "-", "-",
+          "p2_stored", "p2_synced", "p2_loop", "p2_clean", "waited0"]
+NEV = 32  # TL_EVENTS
 
 
 def main() -> None:
@@ -41,7 +43,7 @@ def main() -> None:
                     dtype=torch.bfloat16 if args.out == "bf16" else torch.float32)
     plan = sk.GemmPlan(a, b, c, parse_policy(sk, args.policy), tile)
     grid = plan.g * (tile.blk_m // 128)
-    tl = torch.zeros(grid * 16 + 512, dtype=torch.int64, device="cuda")
+    tl = torch.zeros(grid * NEV + 512, dtype=torch.int64, device="cuda")
     flush = torch.empty(64 << 20, device="cuda")
     for _ in range(3):
         plan.launch()
@@ -57,8 +59,8 @@ def main() -> None:
     torch.cuda.synchronize()
     _lib.lib.skpp_debug_timeline(None)
     raw = tl.cpu().numpy().astype("float64")
-    t = raw[: grid * 16].reshape(grid, 16)
-    ks = raw[grid * 16:].reshape(256, 2)
+    t = raw[: grid * NEV].reshape(grid, NEV)
+    ks = raw[grid * NEV:].reshape(256, 2)
     base = t[:, 0][t[:, 0] > 0].min()
     print(f"{args.m}x{args.n}x{args.k} {args.policy} tile {args.tile} flush={args.flush}: "
           f"event time {e0.elapsed_time(e1) * 1e3:.1f} us, "
@@ -89,7 +91,7 @@ def main() -> None:
                   f"(+{gap:5.0f}) lat {lat:6.0f}")
         if n > 8:
             print(f"  mean arrival spacing k>=8: {(ks[n - 1, 1] - ks[8, 1]) / (n - 9):.0f} cycles")
-    cols = [0, 3, 8, 10, 4, 5, 11, 12, 6]  # start mma_done epi_first part_flag phase1 waited sum1 sum2 phase2
+    cols = [0, 3, 8, 10, 4, 20, 5, 11, 12, 16, 17, 18, 19, 6, 7]  # start mma_done epi_first part_flag phase1 waited0 waited sum1 sum2 p2_stored p2_synced p2_loop p2_clean phase2 end
     if args.per_cta:
         print("  cta      " + " ".join(f"{EVENTS[i][:7]:>7s}" for i in cols))
     for x in range(min(args.per_cta, grid)):
