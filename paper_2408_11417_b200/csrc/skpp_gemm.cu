@@ -438,6 +438,10 @@ enum : int {
   TL_P2_STORED = 16,  // phase 2, thread 0: first band stored to C
   TL_ENTRY = 21,      // thread 0 at kernel entry (before barrier init and griddepcontrol.wait)
   TL_C_TMA = 22,      // SM cycles from griddepcontrol.wait returning to the first A load (thread 0)
+  TL_CP_INIT = 25,    // prologue, SM cycles since entry (thread 0): barriers initialised,
+  TL_CP_TMEM = 26,    //   TMEM allocated and the CTA (pair) synchronised,
+  TL_CP_PREF = 27,    //   first item decoded and its L2 prefetches issued (just before the wait)
+  TL_CP_DEC = 28,     //   first item decoded (before its L2 prefetches)
   TL_CLK_ENTRY = 24,  // clock64 at TL_ENTRY and at TL_END (thread 0): the SM clock rate over the
   TL_CLK_END = 31,    //   kernel against %globaltimer
   TL_EVENTS = 32
@@ -724,9 +728,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t x = blockIdx.x / CG;                      // workgroup (pair) id
   const Sched& s = p.s;
 
+  const long long c_entry = clock64();
   if (threadIdx.x == 0 && p.timeline) {
     SKPP_STAMP(p, TL_ENTRY);
-    p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CLK_ENTRY] = clock64();
+    p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CLK_ENTRY] = c_entry;
   }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -743,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     nsplit_smem[4] = 0u;  // last-starter cleanup (set by the epilogue leader)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_shared();
+    if (p.timeline) p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CP_INIT] = clock64() - c_entry;
   }
   if (warp == 2) {
     if constexpr (CG == 1) {
@@ -767,6 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0 && p.timeline) p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CP_TMEM] = clock64() - c_entry;
   // The producers decode their first item here, before griddepcontrol.wait (it depends only on
   // the kernel parameters), so the first loads issue right after the wait.  While the previous
   // kernel drains, they also pull the first `p.l2_prefetch` k-blocks of it into L2 (A by warp 0,
@@ -779,6 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     cursor_init(pcur, s, x);
     pmore = cursor_next(pcur, s, x, pit);
     if (pmore) tile_rc<RASTER>(s, p.raster, pit.tile, ptm, ptn);
+    if (threadIdx.x == 0 && p.timeline) p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CP_DEC] = clock64() - c_entry;
     if (pmore && p.l2_prefetch) {
       const int32_t m0 = (int32_t)(ptm * TILE_M + rank * kBM);
       const int32_t n0 = (int32_t)(ptn * BN + rank * C::BNC);
@@ -801,6 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Programmatic dependent launch: everything above (barrier init, TMEM
   // allocation, descriptor and L2 prefetch) overlaps the previous kernel's tail;
   // no global memory written by earlier work is read before this wait.
+  if (threadIdx.x == 0 && p.timeline) p.timeline[(uint64_t)blockIdx.x * TL_EVENTS + TL_CP_PREF] = clock64() - c_entry;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const long long c_wait = clock64();
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1051,12 +1060,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_ISSUED);
         // publish: every thread's stores happen-before the barrier; the leader's
-        // gpu-scope release then covers them (release is cumulative).
+        // gpu-scope release then covers them (release is cumulative — CUTLASS's stream-K
+        // barrier publishes the same way).  st.release.gpu already emits the MEMBAR.GPU; an
+        // explicit fence.acq_rel.gpu before it doubled the membar and cost 2-5% per launch on
+        // fixup-bound shapes (decode 16x4096x4096 -4.5%, cfg1 -5%, cfg2 -2.5%, same-box A/B).
         epi_bar_sync();
-        if (leader) {
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          st_release_gpu(p.flags + slot, epoch);
-        }
+        if (leader) st_release_gpu(p.flags + slot, epoch);
         if (leader && n_split == 0) SKPP_STAMP(p, TL_PART_FLAG);
         // the CTA reduces (phase 2) only the tile of its FIRST Stream-K item
         if (sk_seen == 0) split_tiles[n_split++] = it.tile - s.dp_tiles;

@@ -37,6 +37,9 @@ def worker(cases) -> None:
         _lib.lib.skpp_set_cooperative(0)
     if os.environ.get("SKPP_DEBUG"):
         _lib.lib.skpp_set_debug(int(os.environ["SKPP_DEBUG"]))
+    for kv in filter(None, os.environ.get("SKPP_SET", "").split(",")):  # e.g. SKPP_SET=l2_prefetch=4,pdl=0
+        name, val = kv.split("=")
+        getattr(_lib.lib, "skpp_set_" + name)(int(val))
     if os.environ.get("SKPP_AB_CASES"):
         cases = [tuple(int(v) if v.isdigit() else v for v in c.split(":")) for c in os.environ["SKPP_AB_CASES"].split(",")]
     out = {}

@@ -42,6 +42,9 @@ def main() -> None:
 
     if os.environ.get("SKPP_DEBUG"):
         _lib.lib.skpp_set_debug(int(os.environ["SKPP_DEBUG"]))
+    for kv in filter(None, os.environ.get("SKPP_SET", "").split(",")):  # e.g. SKPP_SET=l2_prefetch=4,pdl=0
+        name, val = kv.split("=")
+        getattr(_lib.lib, "skpp_set_" + name)(int(val))
     tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
     m, n, k = args.m, args.n, args.k
     set_bytes = 2 * (m * k + k * n) + 4 * m * n
@@ -80,6 +83,11 @@ def main() -> None:
                 col = (col - base) / 1e3
                 print(f"    {name:>11}: min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f} us")
     for li, tt in enumerate(t):
+        pro = [tt[:, c] for c in (25, 26, 28, 27)]
+        if all((v > 0).any() for v in pro):
+            print(f"  launch {'S-1' if li == 0 else 'S'} prologue (SM cycles since entry, med/max): "
+                  + ", ".join(f"{nm} {np.median(v[v > 0]):.0f}/{v.max():.0f}"
+                              for nm, v in zip(("barriers", "tmem+sync", "decoded", "prefetched"), pro)))
         c_tma = tt[:, 22]
         if (c_tma > 0).any():
             print(f"  launch {'S-1' if li == 0 else 'S'}: SM cycles griddepcontrol.wait -> first A load "
