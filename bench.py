@@ -90,40 +90,68 @@ def load_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled while the timed region runs.
+    """SM clocks and clock-event (throttle) reasons sampled while the timed region runs.
 
-    A reader thread stamps every sample on arrival; ``summary`` keeps the samples
-    that arrived between ``mark_start()`` and ``mark_end()`` (plus one period), so
-    the idle lead-in needed to start nvidia-smi does not dilute the median.
+    NVML (pynvml) is polled every ``period_ms`` from a thread that stamps each sample when
+    it is taken, so even a ~10 ms timed region gets several samples (an ``nvidia-smi -lms``
+    pipe delivers its lines block-buffered, late and in bursts, and left short regions with
+    none).  ``summary`` keeps the samples taken between ``mark_start()`` and ``mark_end()``.
+    Falls back to ``nvidia-smi -lms`` when NVML is unavailable.
     """
 
-    def __init__(self, gpu_index: int, period_ms: int = 20):
-        self.cmd = [
-            "nvidia-smi", f"--id={gpu_index}",
-            "--query-gpu=clocks.sm,clocks.max.sm,power.draw," + ",".join(
-                f"clocks_event_reasons.{r}" for r in REASON_FIELDS),
-            "--format=csv,noheader,nounits", f"-lms={period_ms}",
-        ]
-        self.period = period_ms / 1e3
-        self.proc = None
-        self.samples: list[tuple[float, str]] = []
-        self.t0 = self.t1 = None
+    _NVML_REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                     "sw_power_cap": 0x4}
 
-    def _reader(self):
-        for ln in self.proc.stdout:
-            if ln.strip():
-                self.samples.append((time.time(), ln))
+    def __init__(self, gpu_index: int, period_ms: int = 2):
+        self.gpu = gpu_index
+        self.period = period_ms / 1e3
+        self.samples: list[tuple[float, float, float, int]] = []  # (time, sm MHz, max MHz, reasons)
+        self.t0 = self.t1 = None
+        self.stop = False
+        self.thread = None
+        self.nvml = None
+
+    def _poll(self):
+        nv, h = self.nvml, self.handle
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.time(), float(sm), float(mx), int(rs)))
+            except Exception:  # noqa: BLE001 — a failed poll only loses a sample
+                pass
+            time.sleep(self.period)
+
+    def _poll_smi(self):
+        cmd = ["nvidia-smi", f"--id={self.gpu}", "--query-gpu=clocks.sm,clocks.max.sm," + ",".join(
+            f"clocks_event_reasons.{r}" for r in REASON_FIELDS), "--format=csv,noheader,nounits"]
+        while not self.stop:
+            try:
+                ln = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
+                parts = [p.strip() for p in ln.split(",")]
+                bits = sum(self._NVML_REASONS[r] for r, v in zip(REASON_FIELDS, parts[2:])
+                           if v.lower().startswith("active"))
+                self.samples.append((time.time(), float(parts[0]), float(parts[1]), bits))
+            except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+                pass
 
     def __enter__(self):
         import threading
 
         try:
-            self.proc = subprocess.Popen(self.cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._reader, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
-        time.sleep(0.3)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            target = self._poll
+        except Exception:  # noqa: BLE001 — no NVML: poll nvidia-smi instead
+            self.nvml = None
+            target = self._poll_smi
+        self.thread = threading.Thread(target=target, daemon=True)
+        self.thread.start()
+        time.sleep(0.05)
         return self
 
     def mark_start(self):
@@ -133,38 +161,27 @@ class ClockSampler:
         self.t1 = time.time()
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(max(0.05, 2 * self.period))
-            self.proc.terminate()
+        self.stop = True
+        if self.thread is not None:
+            self.thread.join(timeout=10)
+        if self.nvml is not None:
             try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-            self.thread.join(timeout=5)
+                self.nvml.nvmlShutdown()
+            except Exception:  # noqa: BLE001
+                pass
 
     def summary(self) -> dict:
         t0 = self.t0 if self.t0 is not None else 0.0
-        t1 = (self.t1 if self.t1 is not None else time.time()) + self.period
-        window = [ln for ts, ln in self.samples if t0 <= ts <= t1]
-        if not window:  # region shorter than one period: the first sample after it started
-            window = [ln for ts, ln in self.samples if ts >= t0][:1]
-        sm, mx, reasons = [], [], set()
-        for ln in window:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 3 + len(REASON_FIELDS):
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(REASON_FIELDS, parts[3:]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
+        t1 = self.t1 if self.t1 is not None else time.time()
+        window = [smp for smp in self.samples if t0 <= smp[0] <= t1]
+        if not window:  # region shorter than one poll: the first sample after it started
+            window = [smp for smp in self.samples if smp[0] >= t0][:1]
+        if not window:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = sorted(r for r, bit in self._NVML_REASONS.items() if any(smp[3] & bit for smp in window))
+        return {"sm_mhz": statistics.median(smp[1] for smp in window), "sm_max_mhz": max(smp[2] for smp in window),
+                "reasons": reasons, "samples": len(window),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def physical_gpu(local_rank: int) -> int:

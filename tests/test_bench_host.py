@@ -54,3 +54,19 @@ def test_default_workload_is_cfg3_and_sweep_check_can_be_disabled():
 
     assert bench.WORKLOADS["cfg3"]["n"] == 14336
     assert bench.sweep_check(1, 0, "none", bench.SWEEP_TILE) is None
+
+
+def test_clock_sampler_summary_window_and_reasons():
+    """Samples are stamped when taken; only those inside [mark_start, mark_end] count, and the
+    reason bits map to the names the driver checks (NVML clock-event reason masks)."""
+    import bench
+
+    cs = bench.ClockSampler(0)
+    cs.t0, cs.t1 = 10.0, 10.02
+    cs.samples = [(9.99, 1000.0, 1965.0, 0), (10.005, 1965.0, 1965.0, 0x4), (10.012, 1950.0, 1965.0, 0),
+                  (10.019, 1965.0, 1965.0, 0x40), (10.05, 800.0, 1965.0, 0x8)]
+    out = cs.summary()
+    assert out["samples"] == 3 and out["sm_mhz"] == 1965.0 and out["sm_max_mhz"] == 1965.0
+    assert out["reasons"] == ["hw_thermal_slowdown", "sw_power_cap"]
+    cs.t0, cs.t1 = 10.03, 10.031  # region shorter than one poll: the first sample after its start
+    assert cs.summary()["samples"] == 1 and cs.summary()["reasons"] == ["hw_slowdown"]

@@ -1,7 +1,7 @@
-# round 2 profile: GPU tests, the driver's default bench command (cfg3 + in-run sweep), the
+# round 2 final profile (session 3 kernel): GPU tests, the driver's default bench command (cfg3 + in-run sweep), the
 # reference arm, cfg2 bench, launch list and ncu --set full captures of the selected kernels.
 set -x
-O=gpurun_out/prof2; mkdir -p $O
+O=gpurun_out/prof3; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/nvsmi.txt
 nproc > $O/nproc.txt
 timeout 1500 python -m pytest tests -m gpu -q -rf > $O/gpu_tests.log 2>&1; echo tests rc=$?
@@ -17,3 +17,4 @@ cap() {  # name m n k policy tile dtype
 }
 cap cfg3_256x256x128b16_hybrid1 8192 14336 4096 hybrid1 256x256x128b16 bf16
 cap cfg2_128x128x128_hybrid1 512 512 16384 hybrid1 128x128x128 bf16
+cap decode16_128x128x128_hybrid1 16 4096 4096 hybrid1 128x128x128 bf16

@@ -70,7 +70,8 @@ def main() -> None:
     _lib.lib.skpp_debug_timeline(None)
     torch.cuda.synchronize()
     us_step = e0.elapsed_time(e1) * 1e3 / args.steps
-    t = [b.cpu().numpy()[: grid * NEV].reshape(grid, NEV).astype(np.float64) for b in bufs]
+    raw = [b.cpu().numpy().astype(np.float64) for b in bufs]
+    t = [r[: grid * NEV].reshape(grid, NEV) for r in raw]
     base = t[0][:, 0][t[0][:, 0] > 0].min()
     print(f"{m}x{n}x{k} {args.policy} tile {args.tile}: "
           f"{us_step:.2f} us/step over {args.steps} back-to-back launches ({n_sets} operand sets)")
@@ -99,6 +100,12 @@ def main() -> None:
             lat, tot = bs[okb, 1] - bs[okb, 0], bs[okb, 2] - bs[okb, 0]
             print(f"  launch {'S-1' if li == 0 else 'S'} band_sum (thread 128, SM cycles): first loads back med "
                   f"{np.median(lat):.0f} max {lat.max():.0f}; whole pass med {np.median(tot):.0f} max {tot.max():.0f}")
+    ks = raw[1][grid * NEV: grid * NEV + 512].reshape(256, 2)  # CTA 0 of launch S: (issue, arrival) clock64
+    nk = int((ks[:, 1] > 0).sum())
+    if nk:
+        c0 = t[1][0, 24]  # clock64 at CTA 0's entry
+        print("  launch S, CTA 0 k-blocks (SM cycles since entry: issue / arrival / latency): " + "; ".join(
+            f"{k}: {ks[k, 0] - c0:.0f}/{ks[k, 1] - c0:.0f}/{ks[k, 1] - ks[k, 0]:.0f}" for k in range(min(nk, 16))))
     end_prev = (t[0][:, 7][t[0][:, 7] > 0].max() - base) / 1e3
     start_next = (t[1][:, 0][t[1][:, 0] > 0].min() - base) / 1e3
     start_next_med = (np.median(t[1][:, 0][t[1][:, 0] > 0]) - base) / 1e3
