@@ -369,6 +369,36 @@ def _check_closed_form(sched: Schedule, size: ProblemSize, tile: TileShape) -> N
         )
 
 
+# Plans of execute_schedule calls, keyed by everything the native plan bakes in (device,
+# operand addresses, row strides, dtypes, problem, tile, policy, g).  Repeated calls of one
+# shape get the same device addresses back from torch's caching allocator, so they skip the
+# plan build (three cuTensorMapEncodeTiled calls and the schedule closed form, ~14 us,
+# profiles/round2/e2e_overhead.jsonl).  A cached plan holds no tensor references (the caller's
+# tensors own the memory); it is launched only when live tensors match its key exactly.
+_PLAN_CACHE: "dict[tuple, GemmPlan]" = {}
+_PLAN_CACHE_MAX = 64
+_plan_cache_stats = {"hits": 0, "misses": 0}
+
+
+def _cached_plan(a, b, c, policy, tile, g):
+    key = (a.device.index, a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), c.data_ptr(), c.stride(0),
+           tuple(a.shape), tuple(b.shape), a.dtype, c.dtype, tile, policy, g)
+    with _ws_lock:
+        plan = _PLAN_CACHE.get(key)
+        if plan is not None:
+            _plan_cache_stats["hits"] += 1
+            _PLAN_CACHE[key] = _PLAN_CACHE.pop(key)  # most recently used last
+            return plan
+    plan = GemmPlan(a, b, c, policy, tile, g)
+    plan.a = plan.b = plan.c = None  # the key's tensors own the memory, not the plan
+    with _ws_lock:
+        _plan_cache_stats["misses"] += 1
+        _PLAN_CACHE[key] = plan
+        while len(_PLAN_CACHE) > _PLAN_CACHE_MAX:
+            _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+    return plan
+
+
 def execute_schedule(
     a,
     b,
@@ -432,7 +462,7 @@ def execute_schedule(
     # Padding K or N up to a multiple of 8 never changes ceil(K/blk_k) or
     # ceil(N/blk_n) (the implemented blk_n/blk_k are multiples of 8), so the
     # launched schedule is the caller's; padded K only adds zero products.
-    GemmPlan(ad, bd, c, sched.policy, tile, sched.g).launch()
+    _cached_plan(ad, bd, c, sched.policy, tile, sched.g).launch()
     out = c[:, : size.n]
     if is_torch:
         if not host_result:

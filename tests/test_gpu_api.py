@@ -362,3 +362,26 @@ def test_sweep_cold_timing_rotates_operand_sets():
     m.GemmPlan(a, b, c, m.Policy.hybrid(1), tile).launch()
     torch.cuda.synchronize()
     assert torch.equal(c.double(), a.double() @ b.double())
+
+
+def test_execute_schedule_reuses_plans_for_repeated_shapes():
+    """Repeated execute_schedule calls of one shape skip the plan build (the cached plan is keyed
+    by the operands' device addresses, strides and dtypes, and holds no tensor references);
+    results stay exact, and a different shape or policy builds its own plan."""
+    m = sk()
+    from paper_2408_11417_b200 import executor as ex
+
+    size, tile = m.ProblemSize(256, 512, 1024), m.TileShape(128, 128, 64)
+    a, b, sched = instance(size, tile, 148, m.Policy.hybrid(1), seed=21)
+    want = ogemm.reference_gemm(a, b)
+    at, bt = torch.from_numpy(a).to(torch.bfloat16).pin_memory(), torch.from_numpy(b).to(torch.bfloat16).pin_memory()
+    before = dict(ex._plan_cache_stats)
+    for _ in range(5):
+        got = m.execute_schedule(at, bt, sched, tile, size)
+        assert np.array_equal(got.double().numpy(), want)
+    assert ex._plan_cache_stats["hits"] - before["hits"] >= 3
+    size2 = m.ProblemSize(256, 384, 1024)
+    a2, b2, sched2 = instance(size2, tile, 148, m.Policy.all_stream_k(), seed=22)
+    got2 = m.execute_schedule(a2, b2, sched2, tile, size2)
+    assert np.array_equal(got2, ogemm.reference_gemm(a2, b2))
+    assert len(ex._PLAN_CACHE) <= ex._PLAN_CACHE_MAX

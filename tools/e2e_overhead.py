@@ -19,8 +19,11 @@ def main() -> None:
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200.tiles import parse_tile
 
-    for m, n, k, tl, pol in [(512, 512, 16384, "128x128x128", sk.Policy.hybrid(1)),
-                             (8192, 14336, 4096, "256x256x128b16", sk.Policy.hybrid(1))]:
+    from paper_2408_11417_b200 import executor as ex
+
+    for m, n, k, tl, pol in [(16, 4096, 4096, "128x128x128", sk.Policy.hybrid(1)),
+                             (512, 512, 16384, "128x128x128", sk.Policy.hybrid(1)),
+                             (8192, 14336, 4096, "256x256x128b16", sk.Policy.hybrid(3))]:
         tile = parse_tile(tl)
         a = torch.randn(m, k, device="cuda").to(torch.bfloat16)
         b = torch.randn(k, n, device="cuda").to(torch.bfloat16)
@@ -43,7 +46,8 @@ def main() -> None:
                           "execute_schedule_ms": {"median": round(statistics.median(calls) * 1e3, 3),
                                                   "min": round(min(calls) * 1e3, 3), "max": round(max(calls) * 1e3, 3),
                                                   "p90": round(sorted(calls)[int(0.9 * len(calls))] * 1e3, 3)},
-                          "h2d_bytes": 2 * (m * k + k * n), "d2h_bytes": 4 * m * n}), flush=True)
+                          "h2d_bytes": 2 * (m * k + k * n), "d2h_bytes": 4 * m * n,
+                          "plan_cache": dict(ex._plan_cache_stats)}), flush=True)
         del out
 
 
