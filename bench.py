@@ -413,11 +413,15 @@ def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool,
             tm, tn = divmod(t, n_tiles)
             flops += 2 * (min(bm, m - tm * bm)) * (min(bn, n - tn * bn)) * (min(ke * bk, k) - kb * bk)
     out = []
-    t_start = time.perf_counter()
-    while len(out) < max_reps and (not out or time.perf_counter() - t_start < max_seconds):
-        t0 = time.perf_counter()
-        ogemm.execute_schedule(a, b, sched, m, n, k, bm, bn, bk, n_tiles)
-        out.append((time.perf_counter() - t0, flops))
+    # every host core for OpenBLAS, whatever OMP_NUM_THREADS the launcher set (torchrun sets 1)
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=len(os.sched_getaffinity(0))):
+        t_start = time.perf_counter()
+        while len(out) < max_reps and (not out or time.perf_counter() - t_start < max_seconds):
+            t0 = time.perf_counter()
+            ogemm.execute_schedule(a, b, sched, m, n, k, bm, bn, bk, n_tiles)
+            out.append((time.perf_counter() - t0, flops))
     return out
 
 
@@ -501,11 +505,20 @@ def run_ours(args, wl: dict) -> None:
     import torch
 
     world, rank, local = dist_setup(args.gpus)
+    # Test hook: SKPP_BENCH_SHARED_GPU=1 runs every rank on cuda:0 over gloo, so the N > 1 control
+    # flow (barriers, max-over-ranks, the sharded sweep's gather) can be exercised on a one-GPU box
+    # (NCCL refuses two ranks on one device).  Numbers from such a run are not bench values.
+    shared = os.environ.get("SKPP_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import sweep
 
@@ -563,7 +576,7 @@ def run_ours(args, wl: dict) -> None:
         torch.distributed.barrier()
     total_ms = t_start.elapsed_time(t_end)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cpu" if shared else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     per_step_s = total_ms / args.steps / 1e3
@@ -607,7 +620,7 @@ def run_ours(args, wl: dict) -> None:
     e2e_steps = len(e2e_t)
     e2e_med = statistics.median(e2e_t)
     if world > 1:
-        t = torch.tensor([e2e_med], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_med], dtype=torch.float64, device="cpu" if shared else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_med = float(t.item())
     e2e_value = world * flops / e2e_med / 1e12
@@ -619,8 +632,8 @@ def run_ours(args, wl: dict) -> None:
     if rank == 0:
         cores = len(os.sched_getaffinity(0))
         cpu_runs = cpu_oracle_gemm(wl, policy.kind.value, policy.sk_batches, policy.sk_first,
-                                   max_seconds=args.cpu_seconds, max_reps=20)
-        cpu_value = statistics.median(f / t for t, f in cpu_runs) / 1e12
+                                   max_seconds=args.cpu_seconds, max_reps=20) if world == 1 else []
+        cpu_value = statistics.median(f / t for t, f in cpu_runs) / 1e12 if cpu_runs else None
         per_config = {f"{tl.tile_label(t)}/{p.label}": round(size.flops / (e.makespan * 1e-6) / 1e12, 2)
                       for t, r in rec.per_tile for p, e in r.costs}
         roof = roofline(flops, nbytes, per_step_s, peaks, sustained=total_ms > 100.0)
@@ -670,11 +683,12 @@ def run_ours(args, wl: dict) -> None:
             "roofline": roof,
             "fixup": fixup_summary(plan, tile, policy, args.workload, flops, nbytes, per_step_s),
             "sweep": sweep_block,
+            # the CPU leg runs on rank 0 at N = 1 only (the reference arm times it at every N)
             "cpu_baseline": {
                 "value": round(cpu_value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
                 "sample": f"{len(cpu_runs)} full {m}x{n}x{k} runs of the oracle port of gemmsched "
                           f"execute_schedule (float64 numpy/OpenBLAS, policy {policy.label})",
-            },
+            } if cpu_value is not None else None,
             "e2e": {
                 "value": round(e2e_value, 3), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": int(2 * (m * k + k * n)), "d2h_bytes_per_step": int(4 * m * n),
