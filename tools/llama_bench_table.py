@@ -1,0 +1,146 @@
+#!/usr/bin/env python
+"""BASELINE cfg3 table on the final kernel: Llama-3-8B projections (M = 1..8192 tokens,
+N in {4096, 14336}, K = 4096, bf16), each timed the way bench.py times (K back-to-back launches
+over rotating operand sets larger than L2):
+
+  * selected  — what a user of the shipped bank gets: ``tiles.Selector`` (Bloom candidates +
+                baseline, timed once on the operands, fastest cached), then timed;
+  * DP base   — data-parallel on the bank's baseline tile 128x128x64 (the paper's comparison);
+  * DP best   — the fastest data-parallel over the candidate tiles;
+  * cuBLAS    — torch.matmul into the same output dtype (context, not the reference);
+  * oracle    — min over all 49 (tile, policy) of the final sweep records (warm-L2 CUDA-graph
+                times, ``profiles/round2/sweep_r2_final_records.*.csv``), next to the selected
+                config's time in the same records.
+
+Output: one JSON line per shape and a markdown table (``--md``).  Both sides write ``--out``
+dtype (default bf16, torch.matmul's output type).
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import glob
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+DP_TILES = ["128x128x64", "128x64x128", "128x128x128", "256x256x64", "256x256x128", "256x256x128b16"]
+
+
+def rotate_us(fns, budget_s=0.05):
+    import torch
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for f in fns:
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    est = e0.elapsed_time(e1) / 1e3 / len(fns)
+    for i in range(max(len(fns), int(0.02 / max(est, 1e-6)))):  # ~20 ms of warm-up (clocks, caches)
+        fns[i % len(fns)]()
+    torch.cuda.synchronize()
+    steps = max(2 * len(fns), min(4000, int(budget_s / max(est, 1e-6))))
+    e0.record()
+    for i in range(steps):
+        fns[i % len(fns)]()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / steps
+
+
+def sweep_records():
+    recs = {}
+    for path in glob.glob(os.path.join(ROOT, "profiles", "round2", "sweep_r2_final_records.*.csv")):
+        tile = path.rsplit("records.", 1)[1][:-4]
+        for r in csv.DictReader(open(path)):
+            key = (int(r["m"]), int(r["n"]), int(r["k"]))
+            pol = (int(r["policy_ordinal"]), int(r["sk_batches"]), int(r["sk_first"]))
+            recs.setdefault(key, {})[(tile, pol)] = float(r["makespan"])
+    return recs
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--md", default=None)
+    ap.add_argument("--tokens", default=",".join(str(1 << e) for e in range(14)))
+    args = ap.parse_args()
+
+    import torch
+
+    import paper_2408_11417_b200 as sk
+    from paper_2408_11417_b200 import tiles as tl
+
+    out_dt = torch.bfloat16 if args.out == "bf16" else torch.float32
+    bank = tl.TileBank.load(sk.default_bank_dir())
+    records = sweep_records()
+    rows = []
+    for n in (4096, 14336):
+        for m in (int(v) for v in args.tokens.split(",")):
+            k = 4096
+            size = sk.ProblemSize(m, n, k)
+            set_bytes = 2 * (m * k + k * n) + out_dt.itemsize * m * n
+            sets = max(2, min(32, -(-(512 << 20) // set_bytes)))
+            ops = [(torch.randn(m, k, device="cuda").to(torch.bfloat16),
+                    torch.randn(k, n, device="cuda").to(torch.bfloat16),
+                    torch.empty(m, n, device="cuda", dtype=out_dt)) for _ in range(sets)]
+
+            def ours(tile, pol):
+                plans = [sk.GemmPlan(a, b, c, pol, tile) for a, b, c in ops]
+                return rotate_us([p.launch for p in plans])
+
+            sel = tl.Selector(bank)
+            tile, pol = sel.config(size, *ops[0])
+            t_sel = ours(tile, pol)
+            t_dp = {t: ours(tl.parse_tile(t), sk.Policy.data_parallel()) for t in DP_TILES}
+            t_cub = rotate_us([(lambda a=a, b=b, c=c: torch.matmul(a, b, out=c)) for a, b, c in ops])
+            rec = records.get((m, n, k), {})
+            canon = sk.canonical_policies()
+            oracle = min(rec.values()) if rec else None
+            sel_warm = (rec.get((tl.tile_label(tile), (canon.index(pol), pol.sk_batches, int(pol.sk_first))))
+                        if rec and pol in canon else None)
+            flops = 2.0 * m * n * k
+            best_dp_tile = min(t_dp, key=t_dp.get)
+            row = {"m": m, "n": n, "k": k, "dp_util_128x128": round(sk.dp_utilization(
+                       sk.grid_info(size, sk.TileShape(128, 128, 64)), 148), 3),
+                   "selected": f"{tl.tile_label(tile)}/{pol.label}", "selected_us": round(t_sel, 2),
+                   "selected_tflops": round(flops / t_sel / 1e6, 1),
+                   "dp_base_us": round(t_dp["128x128x64"], 2), "dp_best": best_dp_tile,
+                   "dp_best_us": round(t_dp[best_dp_tile], 2), "cublas_us": round(t_cub, 2),
+                   "vs_dp_base": round(t_dp["128x128x64"] / t_sel, 3),
+                   "vs_dp_best": round(t_dp[best_dp_tile] / t_sel, 3),
+                   "vs_cublas": round(t_cub / t_sel, 3),
+                   "warm_selected_vs_oracle": round(sel_warm / oracle, 3) if oracle and sel_warm else None,
+                   "out": args.out}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+            del ops
+            torch.cuda.empty_cache()
+    if args.md:
+        with open(args.md, "w") as fh:
+            fh.write("| M | N | dp_util (128x128) | selected (tile/policy) | selected us | TFLOP/s | DP 128x128x64 us | "
+                     "best DP (tile) us | cuBLAS us | vs DP base | vs best DP | vs cuBLAS | warm: selected / oracle |\n")
+            fh.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+            for r in rows:
+                fh.write(f"| {r['m']} | {r['n']} | {r['dp_util_128x128']} | {r['selected']} | {r['selected_us']} | "
+                         f"{r['selected_tflops']} | {r['dp_base_us']} | {r['dp_best_us']} ({r['dp_best']}) | "
+                         f"{r['cublas_us']} | {r['vs_dp_base']}x | {r['vs_dp_best']}x | {r['vs_cublas']}x | "
+                         f"{r['warm_selected_vs_oracle']} |\n")
+            wq = [r for r in rows if r["dp_util_128x128"] < 0.9]
+            import math
+
+            gm = lambda xs: math.exp(sum(math.log(v) for v in xs) / len(xs))  # noqa: E731
+            fh.write(f"\nwave-quantisation-bound sizes (dp_util < 0.9): {len(wq)}; selected vs DP on the baseline tile: "
+                     f"geomean {gm([r['vs_dp_base'] for r in wq]):.2f}x, min {min(r['vs_dp_base'] for r in wq):.2f}x; "
+                     f"vs the best DP tile: geomean {gm([r['vs_dp_best'] for r in wq]):.2f}x, "
+                     f"min {min(r['vs_dp_best'] for r in wq):.2f}x; all sizes vs cuBLAS: geomean "
+                     f"{gm([r['vs_cublas'] for r in rows]):.2f}x\n")
+
+
+if __name__ == "__main__":
+    main()
