@@ -62,6 +62,13 @@ constexpr uint32_t kStagingBytes = 4 * 2 * kStageBuf;
 // ever overlapping another plan's partial slots.  Launch e uses the parity e & 1 words and
 // resets the other parity's for launch e + 1 (which starts only after this grid completed).
 constexpr uint32_t kMaxCtas = 1024;
+// Slot-flag value (epoch | kOwnerDone) of an owner item whose tile the owner finished itself in
+// phase 1 (owner reduction, see the epilogue): no partial in the slot, nothing left to reduce.
+// Epochs stay below 2^31 (one per Stream-K launch on a workspace).
+constexpr uint32_t kOwnerDone = 0x80000000u;
+// Bound of the owner's phase-1 wait for the other contributor's partial (~4 us): the liveness
+// protocol needs every wait in phase 1 to be bounded; on timeout the owner publishes its partial.
+constexpr long long kOwnerWaitCycles = 8000;
 constexpr uint64_t kWsFlagsOff = 1024;
 constexpr uint64_t kWsStatesOff = kWsFlagsOff + 2ull * kMaxCtas * 4;
 constexpr uint64_t kWsCtlBytes = 32768;
@@ -559,6 +566,19 @@ __device__ __forceinline__ bool wait_flag_until(const uint32_t* flag, uint32_t e
   return true;
 }
 
+// Owner flag of a split tile in phase 2: 1 = the owner's partial is published, 2 = the owner
+// finished the tile itself in phase 1 (epoch | kOwnerDone), 0 = neither within `cycles`.
+__device__ __forceinline__ uint32_t wait_owner_flag(const uint32_t* flag, uint32_t epoch, long long t0,
+                                                   uint32_t cycles) {
+  while (true) {
+    const uint32_t v = ld_acquire_gpu(flag);
+    if (v == epoch) return 1u;
+    if (v == (epoch | kOwnerDone)) return 2u;
+    if (clock64() - t0 > (long long)cycles) return 0u;
+    __nanosleep(32);
+  }
+}
+
 // Header words of the liveness protocol (phase 2), per parity of the launch epoch.
 constexpr uint32_t kHdrStarted = 8;   // hdr[8 + par]: CTAs of the launch that have started
 constexpr uint32_t kHdrAbandon = 16;  // hdr[16 + par]: some band of the launch was abandoned
@@ -1007,7 +1027,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader && rank == 0) record_item(p, x, local, it, tm_, tn_);
       const uint64_t tile_row0 = tm_ * TILE_M + rank * kBM;
       const uint64_t tile_col0 = tn_ * BN;
-      if (partial) {
+      // Owner reduction (fp32 C).  A split tile with exactly two contributors whose owner item is
+      // this workgroup's LAST Stream-K item (its range began in an earlier tile) is finished
+      // here instead of at the end of the launch: the other contributor x+1 holds the rest of the
+      // tile as its FIRST Stream-K item, published long before this item completes, so the
+      // epilogue adds that partial to its accumulator and stores C — (0 + p[x+1]) + p[x], the
+      // phase-2 order, so the bits are identical — while the MMA moves on to the next item.  No
+      // partial of this item is written, and x+1 skips the tile in phase 2 (the slot flag says
+      // epoch | kOwnerDone).  The wait for x+1 is bounded (liveness); on timeout this item
+      // publishes its partial as usual.
+      bool reduce_peer = false;
+      if (partial && it.role == ROLE_OWNER && it.peer_hi == (uint64_t)x + 1 && sk_seen >= 1 && !out16 &&
+          !(p.debug & 16u)) {
+        if (leader) {
+          const uint32_t* pf = p.flags + 2ull * ((uint64_t)(x + 1) * CG + rank);
+          uint32_t ok = 0;
+          const long long t0 = clock64();
+          while (true) {
+            if (ld_acquire_gpu(pf) == epoch) {
+              ok = 1;
+              break;
+            }
+            if (clock64() - t0 > kOwnerWaitCycles) break;
+            __nanosleep(32);
+          }
+          nsplit_smem[9] = ok;  // one owner item per workgroup at most: the word is written once
+        }
+        epi_bar_sync();  // the decision, and the peer partial (acquired by the leader), for all
+        reduce_peer = nsplit_smem[9] != 0u;
+      }
+      if (partial && !reduce_peer) {
         // Partial slot layout: float4[BN/4][BM] ("column-group major"): a warp's
         // store of one column group is 32 consecutive rows = 512 contiguous bytes,
         // and a contributor's share of columns is one contiguous range.
@@ -1085,6 +1134,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               w[j] = pack2(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]), p.out_dtype);
               w[16 + j] = pack2(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]), p.out_dtype);
             }
+          } else if (reduce_peer) {
+            // the other contributor's 32 columns of this row (column groups c*8 .. c*8+7 of its
+            // slot, float4[BN/4][128]), loaded before the TMEM read so the L2 latency overlaps
+            const float4* src = reinterpret_cast<const float4*>(p.ws) +
+                                (2ull * ((uint64_t)(x + 1) * CG + rank)) * (uint64_t)(kBM * (BN / 4)) +
+                                (uint64_t)(c * 8) * kBM + row;
+            float4 q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = ld_cg_f4(src + (uint64_t)j * kBM);
+            tmem_ld_32(taddr + c * 32, w);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              w[4 * j] = __float_as_uint((0.f + q[j].x) + __uint_as_float(w[4 * j]));
+              w[4 * j + 1] = __float_as_uint((0.f + q[j].y) + __uint_as_float(w[4 * j + 1]));
+              w[4 * j + 2] = __float_as_uint((0.f + q[j].z) + __uint_as_float(w[4 * j + 2]));
+              w[4 * j + 3] = __float_as_uint((0.f + q[j].w) + __uint_as_float(w[4 * j + 3]));
+            }
           } else {
             tmem_ld_32(taddr + c * 32, w);
             tmem_ld_wait();
@@ -1120,6 +1187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             store_row_direct(p, tile_row0 + row, tile_col0 + c * ccols, w);
           }
         }
+        if (reduce_peer && leader) st_release_gpu(p.flags + slot, epoch | kOwnerDone);
       }
       if (it.phase == PHASE_SK) ++sk_seen;
       ++local;
@@ -1231,7 +1299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t want = nc - 1;
           uint32_t ready = 0;
           while (true) {
-            if (ld_acquire_gpu(p.flags + slot0) == epoch) { ready = 1; break; }
+            const uint32_t v = ld_acquire_gpu(p.flags + slot0);
+            if (v == epoch) { ready = 1; break; }
+            if (v == (epoch | kOwnerDone)) { ready = 2; break; }  // finished by the owner
             if (*peers_seen >= want || p2w[0] != 0u) break;
             if (clock64() - t0 > (long long)limit) {
               atomicOr(const_cast<uint32_t*>(p2w), 1u);
@@ -1252,6 +1322,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         limit = 0xFFFFFFFFu;
       }
       if (stamps) SKPP_STAMP(p, TL_WAITED);
+      if (p2w[2] == 2u) {  // the owner reduced the tile in phase 1 (owner reduction): nothing to do
+        phase2_bar_sync();
+        return;
+      }
       const bool owner_ready = p2w[2] != 0u && !(p.debug & 1u);
       const uint32_t nrows = R1 - R0;
       band_reduce<CG, V>(ra, R0, nrows, Vv, 0, owner_ready ? nc : nc - 1, false, stage, ft);
@@ -1259,16 +1333,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!owner_ready) {
         if (ft == 0) {
           uint32_t go = 1u;
-          if (!wait_flag_until(p.flags + slot0, epoch, clock64(), limit)) {
+          uint32_t got = wait_owner_flag(p.flags + slot0, epoch, clock64(), limit);
+          if (got == 0u) {
             go = abandon_or_wait(p.hdr, par, bst);
-            if (go) wait_flag(p.flags + slot0, epoch);
+            if (go) got = wait_owner_flag(p.flags + slot0, epoch, clock64(), 0xFFFFFFFFu);
           }
           p2w[1] = go;
+          p2w[2] = got;
         }
         phase2_bar_sync();  // also orders the stage writes above before the re-reads below
-        if (p2w[1] == 0u) {
+        if (p2w[1] == 0u || p2w[2] == 2u) {
           phase2_bar_sync();
-          return;  // handed to the last starter (the peers' partial sums are discarded)
+          return;  // handed to the last starter, or finished by the owner (peer sums discarded)
         }
         band_reduce<CG, V>(ra, R0, nrows, Vv, nc - 1, nc, true, stage, ft);
         if (stamps) SKPP_STAMP(p, TL_SUM2);

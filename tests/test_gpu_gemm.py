@@ -320,3 +320,47 @@ def test_banded_tile_order_bitwise_every_policy(band, m, n, k, tile):
         got, plan = _run(a, b, pol, t, trace_cap=64)
         assert np.array_equal(got.double().cpu().numpy(), want), (band, pol.label)
         _assert_trace(plan, m, n, k, tile, pol, band)
+
+
+@pytest.mark.parametrize("m,n,k,tile,pol", [
+    (2048, 2560, 1096, (128, 128, 64), ("hybrid", 2, True)),      # multi-wave, two-contributor split tiles
+    (1024, 14336, 1024, (256, 256, 128, 16), ("hybrid", 3, True)),  # banded CTA pair (cfg3-like hybrid)
+    (1536, 2048, 4096, (128, 128, 128), ("hybrid", 2, False)),    # DP-first: Stream-K items last
+])
+def test_owner_reduction_bit_identical_to_phase2_path(m, n, k, tile, pol):
+    """Owner reduction: a split tile with two contributors whose owner item is the owner's last
+    Stream-K item is finished in the owner's epilogue ((0 + p[x+1]) + p[x]) instead of in phase 2.
+    The path must be taken (slot flags carry epoch | 0x80000000), give the same bits as the
+    phase-2 reduction (skpp_set_debug bit 4 disables it) on randn inputs, and be exact on
+    integer inputs."""
+    sk = _sk()
+    from paper_2408_11417_b200 import _lib
+
+    t = sk.kernel_tile(*tile) if len(tile) == 4 else sk.TileShape(*tile)
+    policy = sk.Policy.hybrid(pol[1], sk_first=pol[2])
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(m + n)
+    ar = torch.randn(m, k, generator=gen, device="cuda").to(torch.bfloat16)
+    br = torch.randn(k, n, generator=gen, device="cuda").to(torch.bfloat16)
+    outs = []
+    try:
+        for flags in (16, 0):
+            _lib.lib.skpp_set_debug(flags)
+            c = torch.full((m, n), float("nan"), device="cuda")
+            plan = sk.GemmPlan(ar, br, c, policy, t)
+            plan.launch()
+            torch.cuda.synchronize()
+            outs.append(c)
+            if flags == 0:
+                ws = next(iter(plan._ws_cache.values()))[2]
+                hdr = ws[:64].view(torch.int32).cpu()
+                epoch = int(hdr[0])
+                n_slots = 2 * plan.g * (tile[0] // 128)
+                words = ws[1024:1024 + 4 * n_slots].view(torch.int32).cpu().numpy().view(np.uint32)
+                assert int((words == (epoch | 0x80000000)).sum()) > 0, "owner reduction never taken"
+    finally:
+        _lib.lib.skpp_set_debug(0)
+    assert torch.equal(outs[0], outs[1])
+    a, b = _int_case(m, n, k, seed=k)
+    got, _ = _run(a, b, policy, t)
+    assert np.array_equal(got.double().cpu().numpy(), ogemm.reference_gemm(a, b))
