@@ -1027,7 +1027,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader && rank == 0) record_item(p, x, local, it, tm_, tn_);
       const uint64_t tile_row0 = tm_ * TILE_M + rank * kBM;
       const uint64_t tile_col0 = tn_ * BN;
-      // Owner reduction (fp32 C).  A split tile with exactly two contributors whose owner item is
+      // Owner reduction.  A split tile with exactly two contributors whose owner item is
       // this workgroup's LAST Stream-K item (its range began in an earlier tile) is finished
       // here instead of at the end of the launch: the other contributor x+1 holds the rest of the
       // tile as its FIRST Stream-K item, published long before this item completes, so the
@@ -1037,8 +1037,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // epoch | kOwnerDone).  The wait for x+1 is bounded (liveness); on timeout this item
       // publishes its partial as usual.
       bool reduce_peer = false;
-      if (partial && it.role == ROLE_OWNER && it.peer_hi == (uint64_t)x + 1 && sk_seen >= 1 && !out16 &&
-          !(p.debug & 16u)) {
+      if (partial && it.role == ROLE_OWNER && it.peer_hi == (uint64_t)x + 1 && sk_seen >= 1 && !(p.debug & 16u)) {
         if (leader) {
           const uint32_t* pf = p.flags + 2ull * ((uint64_t)(x + 1) * CG + rank);
           uint32_t ok = 0;
@@ -1129,6 +1128,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld_32(taddr + c * 64, r0);
             tmem_ld_32(taddr + c * 64 + 32, r1);
             tmem_ld_wait();
+            if (reduce_peer) {  // owner reduction: add the other contributor's 64 columns, 32 at a time
+              const float4* src = reinterpret_cast<const float4*>(p.ws) +
+                                  (2ull * ((uint64_t)(x + 1) * CG + rank)) * (uint64_t)(kBM * (BN / 4)) +
+                                  (uint64_t)(c * 16) * kBM + row;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                uint32_t* r = h ? r1 : r0;
+                float4 q[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) q[j] = ld_cg_f4(src + (uint64_t)(h * 8 + j) * kBM);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  r[4 * j] = __float_as_uint((0.f + q[j].x) + __uint_as_float(r[4 * j]));
+                  r[4 * j + 1] = __float_as_uint((0.f + q[j].y) + __uint_as_float(r[4 * j + 1]));
+                  r[4 * j + 2] = __float_as_uint((0.f + q[j].z) + __uint_as_float(r[4 * j + 2]));
+                  r[4 * j + 3] = __float_as_uint((0.f + q[j].w) + __uint_as_float(r[4 * j + 3]));
+                }
+              }
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               w[j] = pack2(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]), p.out_dtype);

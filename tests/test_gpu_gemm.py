@@ -322,12 +322,13 @@ def test_banded_tile_order_bitwise_every_policy(band, m, n, k, tile):
         _assert_trace(plan, m, n, k, tile, pol, band)
 
 
+@pytest.mark.parametrize("out", ["fp32", "bf16"])
 @pytest.mark.parametrize("m,n,k,tile,pol", [
     (2048, 2560, 1096, (128, 128, 64), ("hybrid", 2, True)),      # multi-wave, two-contributor split tiles
     (1024, 14336, 1024, (256, 256, 128, 16), ("hybrid", 3, True)),  # banded CTA pair (cfg3-like hybrid)
     (1536, 2048, 4096, (128, 128, 128), ("hybrid", 2, False)),    # DP-first: Stream-K items last
 ])
-def test_owner_reduction_bit_identical_to_phase2_path(m, n, k, tile, pol):
+def test_owner_reduction_bit_identical_to_phase2_path(m, n, k, tile, pol, out):
     """Owner reduction: a split tile with two contributors whose owner item is the owner's last
     Stream-K item is finished in the owner's epilogue ((0 + p[x+1]) + p[x]) instead of in phase 2.
     The path must be taken (slot flags carry epoch | 0x80000000), give the same bits as the
@@ -346,7 +347,8 @@ def test_owner_reduction_bit_identical_to_phase2_path(m, n, k, tile, pol):
     try:
         for flags in (16, 0):
             _lib.lib.skpp_set_debug(flags)
-            c = torch.full((m, n), float("nan"), device="cuda")
+            c = torch.full((m, n), float("nan"), device="cuda",
+                           dtype=torch.float32 if out == "fp32" else torch.bfloat16)
             plan = sk.GemmPlan(ar, br, c, policy, t)
             plan.launch()
             torch.cuda.synchronize()
@@ -360,7 +362,9 @@ def test_owner_reduction_bit_identical_to_phase2_path(m, n, k, tile, pol):
                 assert int((words == (epoch | 0x80000000)).sum()) > 0, "owner reduction never taken"
     finally:
         _lib.lib.skpp_set_debug(0)
-    assert torch.equal(outs[0], outs[1])
-    a, b = _int_case(m, n, k, seed=k)
-    got, _ = _run(a, b, policy, t)
-    assert np.array_equal(got.double().cpu().numpy(), ogemm.reference_gemm(a, b))
+    assert torch.equal(outs[0].view(torch.int16 if out == "bf16" else torch.int32),
+                       outs[1].view(torch.int16 if out == "bf16" else torch.int32))  # bits, incl. signed zeros
+    if out == "fp32":
+        a, b = _int_case(m, n, k, seed=k)
+        got, _ = _run(a, b, policy, t)
+        assert np.array_equal(got.double().cpu().numpy(), ogemm.reference_gemm(a, b))
