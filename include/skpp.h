@@ -186,6 +186,8 @@ void skpp_set_l2_hints(int enable);
    (peers first, owner added in a second pass) even when the owner is already published;
    bit 1 sets the phase-2 wait bound to 0, so every wait not already satisfied takes the
    timeout decision (keep waiting if every CTA started, else abandon to the last starter);
+   bit 4 turns the owner reduction off (two-contributor split tiles whose owner item is the
+   owner's last Stream-K item are then reduced in phase 2 like every other split tile);
    results are bit-identical to the normal path by construction (tests check it). */
 void skpp_set_debug(int flags);
 /* Test hook for the liveness tests: launch `ctas` single-warp CTAs with `smem_bytes` of
