@@ -1256,7 +1256,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float4* wsv = reinterpret_cast<const float4*>(p.ws);
     const uint64_t slot_v = (uint64_t)kBM * V;  // float4 per slot
     volatile uint32_t* peers_seen = nsplit_smem + 2;
-    volatile uint32_t* p2w = nsplit_smem + 5;  // [0] a wait timed out, [1] decision, [2] owner ready, [3] claims
+    volatile uint32_t* p2w = nsplit_smem + 5;  // [0] a wait timed out, [1] decision, [2] owner ready, [3] claims,
+                                               // [5] owner flag of the second pass (= nsplit_smem[10]; [9] is the
+                                               // phase-1 owner-reduction decision)
     const uint32_t stage = smem_u32(smem);     // idle operand ring: float4 [row][V+1]
     // Reduce reducer (xr, rk)'s band of split tile u and store it to C.  `bounded`: flag
     // waits may time out and hand the band to the last starter (the CTA's own band);
@@ -1357,10 +1359,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (go) got = wait_owner_flag(p.flags + slot0, epoch, clock64(), 0xFFFFFFFFu);
           }
           p2w[1] = go;
-          p2w[2] = got;
+          p2w[5] = got;  // not p2w[2]: other threads may still be reading it (owner_ready)
         }
         phase2_bar_sync();  // also orders the stage writes above before the re-reads below
-        if (p2w[1] == 0u || p2w[2] == 2u) {
+        if (p2w[1] == 0u || p2w[5] == 2u) {
           phase2_bar_sync();
           return;  // handed to the last starter, or finished by the owner (peer sums discarded)
         }

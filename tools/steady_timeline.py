@@ -45,7 +45,9 @@ def main() -> None:
     for kv in filter(None, os.environ.get("SKPP_SET", "").split(",")):  # e.g. SKPP_SET=l2_prefetch=4,pdl=0
         name, val = kv.split("=")
         getattr(_lib.lib, "skpp_set_" + name)(int(val))
-    tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
+    from paper_2408_11417_b200.tiles import parse_tile
+
+    tile = parse_tile(args.tile)  # "256x256x128b16" = banded tile order 16
     m, n, k = args.m, args.n, args.k
     set_bytes = 2 * (m * k + k * n) + 4 * m * n
     n_sets = max(2, -(-(512 << 20) // set_bytes))

@@ -36,7 +36,9 @@ def main() -> None:
         _lib.lib.skpp_set_debug(int(os.environ["SKPP_DEBUG"]))
     from tools.profile_gemm import parse_policy
 
-    tile = sk.TileShape(*(int(v) for v in args.tile.split("x")))
+    from paper_2408_11417_b200.tiles import parse_tile
+
+    tile = parse_tile(args.tile)  # "256x256x128b16" = banded tile order 16
     a = torch.randn(args.m, args.k, device="cuda").to(torch.bfloat16)
     b = torch.randn(args.k, args.n, device="cuda").to(torch.bfloat16)
     c = torch.empty(args.m, args.n, device="cuda",
