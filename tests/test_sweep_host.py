@@ -225,3 +225,22 @@ def test_snap_corners_encloses_the_size():
     bank.insert(sk.ProblemSize(512, 64, 4), (t0, sk.Policy.hybrid(2)))
     assert (t0, sk.Policy.hybrid(2)) in bank.candidates(z, nearest="corners")
     assert bank.candidates(z, nearest=False) == [bank.baseline]
+
+
+def test_cold_sets_cover_operand_sets_up_to_two_and_a_half_l2():
+    """Cold timing: sets that fit in L2 rotate over >= 4x L2 in total; sets up to 2.5x L2 (e.g.
+    the Llama 14336 x 4096 projections, whose B alone is 117 MB) rotate over two, so one set's
+    B is not re-read from L2 by the next launch; larger sets are timed as they come (HBM)."""
+    p = sw.MeasureParams(cold=True)
+    l2 = sw.L2_BYTES
+    nbytes = lambda z: 2 * (z.m * z.k + z.k * z.n) + 4 * z.m * z.n  # noqa: E731
+    small = sk.ProblemSize(512, 2048, 2048)
+    n = sw.cold_sets(small, p)
+    assert 2 <= n <= p.cold_max_sets and n * nbytes(small) >= 4 * l2
+    for m in (1024, 2048):
+        z = sk.ProblemSize(m, 14336, 4096)
+        assert l2 < nbytes(z) and 2 * nbytes(z) <= 5 * l2
+        assert sw.cold_sets(z, p) == 2
+    assert sw.cold_sets(sk.ProblemSize(8192, 14336, 4096), p) == 0
+    assert sw.cold_sets(sk.ProblemSize(16, 64, 64), p) == 0  # below cold_min_bytes
+    assert sw.cold_sets(small, sw.MeasureParams()) == 0  # cold off
