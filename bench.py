@@ -164,6 +164,12 @@ class ClockSampler:
         self.t1 = time.time()
 
     def __exit__(self, *exc):
+        # a region shorter than the poller's period (or one during which the poller did not get
+        # the GIL) may end before any sample was taken after it started: wait for one (<= 0.5 s)
+        deadline = time.time() + 0.5
+        while (self.t0 is not None and self.thread is not None and self.thread.is_alive()
+               and not any(smp[0] >= self.t0 for smp in self.samples) and time.time() < deadline):
+            time.sleep(0.002)
         self.stop = True
         if self.thread is not None:
             self.thread.join(timeout=10)

@@ -70,3 +70,28 @@ def test_clock_sampler_summary_window_and_reasons():
     assert out["reasons"] == ["hw_thermal_slowdown", "sw_power_cap"]
     cs.t0, cs.t1 = 10.03, 10.031  # region shorter than one poll: the first sample after its start
     assert cs.summary()["samples"] == 1 and cs.summary()["reasons"] == ["hw_slowdown"]
+
+
+def test_clock_sampler_exit_waits_for_a_sample_after_the_region_started():
+    """A timed region shorter than one poll (or one during which the poller did not run) still
+    gets a sample: __exit__ waits (bounded) for the first sample taken after mark_start."""
+    import threading
+    import time
+
+    import bench
+
+    cs = bench.ClockSampler(0)
+
+    def late_poll():
+        time.sleep(0.05)
+        cs.samples.append((time.time(), 1950.0, 1965.0, 0))
+        while not cs.stop:
+            time.sleep(0.002)
+
+    cs.thread = threading.Thread(target=late_poll, daemon=True)
+    cs.thread.start()
+    cs.mark_start()
+    cs.mark_end()
+    cs.__exit__(None, None, None)
+    out = cs.summary()
+    assert out["samples"] == 1 and out["sm_mhz"] == 1950.0
