@@ -51,7 +51,8 @@ def partial(rounds: int, hold: int, seed: int) -> int:
     import paper_2408_11417_b200 as sk
     from paper_2408_11417_b200 import _lib
 
-    ab, bb, want = _operands(seed)
+    shape = os.environ.get("SKPP_LIVENESS_SHAPE")  # "m,n,k" (diagnostics; default 512x512x8192)
+    ab, bb, want = _operands(seed, *map(int, shape.split(","))) if shape else _operands(seed)
     s_hold, s_gemm, s_rel = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     cases = [(sk.Policy.all_stream_k(), sk.TileShape(128, 128, 64)),
              (sk.Policy.hybrid(1), sk.TileShape(128, 128, 128)),
