@@ -124,7 +124,9 @@ uint64_t skpp_workspace_bytes(const skpp_problem_t* p, const skpp_tile_t* t, uin
    {16,32,64,128}; blk_m == 256 (CTA pair) with blk_n in {128,256}, blk_k in {32,64,128}. */
 int skpp_tile_supported(const skpp_tile_t* t);
 /* Persistent Stream-K++ GEMM C = A @ B on the current device, stream-ordered.
-   The workspace must be zero-filled the first time it is used; afterwards the
+   The workspace must be zero-filled the first time it is used, and the fill must have
+   completed (e.g. cudaMemset, or cudaMemsetAsync + a stream sync) before that first launch
+   (Stream-K launches use programmatic dependent launch); afterwards the
    kernel keeps it consistent itself (epoch-tagged flags), so one workspace
    serves any number of stream-ordered launches, including CUDA-graph replays.  trace/trace_counts may be
    NULL; otherwise each CTA x writes up to trace_cap items at

@@ -146,10 +146,18 @@ def _new_workspace(nbytes: int, device: int, stream_handle: int) -> torch.Tensor
     allocation, so no partial slot ever holds recycled memory.  Allocating and zeroing on the
     stream the kernel runs on (not torch's current stream) orders the memset before the
     first launch and ties the block's lifetime to that stream.
+
+    Outside a graph capture the device is then synchronised once, so the fill has landed
+    before the first launch can start.  Stream order alone was not enough: in about 1 of 125
+    fresh processes the first Stream-K launch (programmatic dependent launch, right behind the
+    fill) ran concurrently with the fill, which zeroed the epoch header and the early slots
+    under it (`profiles/round2/session5/`).  The cost is one host sync per new workspace.
     """
     size = max(nbytes, 1 << 20)
     with torch.cuda.stream(torch.cuda.ExternalStream(stream_handle, device=f"cuda:{device}")):
         buf = torch.zeros(size, dtype=torch.uint8, device=f"cuda:{device}")
+    if not _is_capturing(stream_handle):
+        torch.cuda.synchronize(device)
     return buf
 
 
