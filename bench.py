@@ -409,7 +409,8 @@ def cpu_oracle_gemm(wl: dict, policy_kind: str, sk_batches: int, sk_first: bool,
     rng = np.random.default_rng(seed)
     a = ogemm.random_int_matrix(m, k, rng)
     b = ogemm.random_int_matrix(k, n, rng)
-    g = 148 // (bm // 128)  # one workgroup per SM, or per SM pair for 256-row tiles
+    # the tile's declared grid, else one workgroup per SM (per SM pair for 256-row tiles)
+    g = wl.get("g") or 148 // (bm // 128)
     sched = osched.build_schedule(m, n, k, bm, bn, bk, g, policy_kind, sk_batches, sk_first)
     sched = sched[::wg_stride]
     n_tiles = -(-n // bn)
@@ -455,8 +456,8 @@ def run_reference(args, wl: dict) -> None:
     m, n, k = wl["m"], wl["n"], wl["k"]
     size = sk.ProblemSize(m, n, k)
     (tile, policy), cand = host_selection(size, wl["dtype"])
-    g = 148 // (tile.blk_m // 128)
-    wlt = dict(wl, tile=(tile.blk_m, tile.blk_n, tile.blk_k))
+    g = sk.tile_grid(tile) or 148 // (tile.blk_m // 128)
+    wlt = dict(wl, tile=(tile.blk_m, tile.blk_n, tile.blk_k), g=g)
     pol = _policy_tuple(policy)
     # One probe run of a 1/16 sample sizes the per-step sample so the whole --steps/--warmup
     # run stays within a few minutes: full schedule when a step fits CPU_STEP_BUDGET_S.
@@ -478,8 +479,7 @@ def run_reference(args, wl: dict) -> None:
         "config": _config_keys(wl, tile, g, policy.label, args.gpus),
         "selection": {"how": "host-side: shipped tile bank candidates (corners + calibrated prior), "
                              "calibrated-model pick among them (no GPU)",
-                      "candidates": [f"{t.blk_m}x{t.blk_n}x{t.blk_k}" + (f"b{t.band_rows}" if getattr(t, 'band_rows', 0) else "")
-                                     + f"/{p.label}" for t, p in cand]},
+                      "candidates": [f"{sk.tiles.tile_label(t)}/{p.label}" for t, p in cand]},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": sample},
@@ -538,7 +538,7 @@ def run_ours(args, wl: dict) -> None:
     pool = sweep.OperandPool([size], in_dtype, torch.float32, seed=rank)
     tile, policy, rec, cand = select_config(size, cand_tiles, pool)
     g = sk.executor.default_g(tile)
-    wl = dict(wl, tile=(tile.blk_m, tile.blk_n, tile.blk_k))
+    wl = dict(wl, tile=(tile.blk_m, tile.blk_n, tile.blk_k), g=g)
     a, b, c = pool.views(size)
     plan = sk.GemmPlan(a, b, c, policy, tile, g)
     flops = 2.0 * m * n * k

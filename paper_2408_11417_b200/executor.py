@@ -33,7 +33,7 @@ import numpy as np
 
 from . import _lib
 from .scheduler import Schedule, build_schedule, closed_form, grid_info
-from .types import HardwareModel, Policy, ProblemSize, TileShape
+from .types import HardwareModel, Policy, ProblemSize, TileShape, tile_grid
 
 try:
     import torch
@@ -127,9 +127,9 @@ def max_coresident(tile: TileShape) -> int:
 
 
 def default_g(tile: TileShape, device: int | None = None) -> int:
-    """Persistent workgroups of one launch: one CTA per SM, or one CTA pair per
-    two SMs for 256-row (cta_group::2) tiles."""
-    return sm_count(device) // (2 if tile.blk_m == 256 else 1)
+    """Persistent workgroups of one launch: the tile's declared grid (``KernelTile.grid``),
+    else one CTA per SM, or one CTA pair per two SMs for 256-row (cta_group::2) tiles."""
+    return tile_grid(tile) or sm_count(device) // (2 if tile.blk_m == 256 else 1)
 
 
 def tile_supported(tile: TileShape) -> bool:

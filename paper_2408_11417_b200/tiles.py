@@ -28,7 +28,7 @@ from dataclasses import dataclass
 
 from .costmodel import Calibration, CostEstimate, TuneRecord, rank_costs
 from .sieve import SieveBank
-from .types import Policy, ProblemSize, TileShape, kernel_tile, tile_order
+from .types import Policy, ProblemSize, TileShape, kernel_tile, tile_grid, tile_order
 
 Config = tuple  # (TileShape, Policy)
 
@@ -42,15 +42,17 @@ def default_bank_dir() -> str:
 
 
 def tile_label(t: TileShape) -> str:
-    """``MxNxK`` for the reference's tile order, ``MxNxKbG`` for G-row bands (KernelTile)."""
-    band = tile_order(t)
-    return f"{t.blk_m}x{t.blk_n}x{t.blk_k}" + (f"b{band}" if band else "")
+    """``MxNxK`` for the reference's tile order on one workgroup per SM; ``bG`` appends G-row
+    bands, ``gN`` a persistent grid of N workgroups (KernelTile)."""
+    band, grid = tile_order(t), tile_grid(t)
+    return f"{t.blk_m}x{t.blk_n}x{t.blk_k}" + (f"b{band}" if band else "") + (f"g{grid}" if grid else "")
 
 
 def parse_tile(s: str) -> TileShape:
     """Inverse of :func:`tile_label`."""
-    dims, _, band = s.partition("b")
-    return kernel_tile(*(int(v) for v in dims.split("x")), int(band) if band else 0)
+    rest, _, grid = s.partition("g")
+    dims, _, band = rest.partition("b")
+    return kernel_tile(*(int(v) for v in dims.split("x")), int(band) if band else 0, int(grid) if grid else 0)
 
 
 @dataclass(frozen=True)

@@ -295,6 +295,27 @@ def test_kernel_tile_labels_round_trip():
         sk.KernelTile(256, 256, 128, 0)
 
 
+def test_kernel_tile_grid_parameter():
+    """KernelTile.grid: a declared persistent grid (label suffix gN) that default_g honours; the
+    schedule is the reference's build_schedule for HardwareModel(grid, 1)."""
+    from paper_2408_11417_b200 import tiles
+    from paper_2408_11417_b200.executor import default_g
+
+    for lab in ("128x128x128g128", "128x64x128g144", "256x256x128b16g64"):
+        t = tiles.parse_tile(lab)
+        assert tiles.tile_label(t) == lab
+        assert sk.tile_grid(t) == int(lab.split("g")[1])
+        assert default_g(t) == sk.tile_grid(t)  # no device query when the grid is declared
+    t = tiles.parse_tile("128x128x128g128")
+    assert sk.tile_order(t) == 0 and t != sk.TileShape(128, 128, 128)
+    ref = sk.build_schedule(sk.ProblemSize(512, 512, 16384), sk.TileShape(128, 128, 128), sk.HardwareModel(128, 1),
+                            sk.Policy.hybrid(1))
+    assert sk.build_schedule(sk.ProblemSize(512, 512, 16384), t, sk.HardwareModel(128, 1),
+                             sk.Policy.hybrid(1)).assignments == ref.assignments
+    with pytest.raises(ValueError):
+        sk.KernelTile(128, 128, 128, 0, 0)
+
+
 def test_coverage_audit_matches_reference():
     for rec in GOLD["coverage"]:
         mt, nt, ipt, tt, ti = rec["grid"]
