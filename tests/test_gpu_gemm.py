@@ -322,6 +322,26 @@ def test_banded_tile_order_bitwise_every_policy(band, m, n, k, tile):
         _assert_trace(plan, m, n, k, tile, pol, band)
 
 
+@pytest.mark.parametrize("grid", [64, 128, 144])
+@pytest.mark.parametrize("m,n,k,tile", [
+    (512, 512, 16384, (128, 128, 128)),   # cfg2: 16 tiles x 128 k-iterations
+    (16, 4096, 4096, (128, 128, 128)),    # decode-like
+    (1024, 1024, 1024, (128, 64, 128)),   # 128 tiles x 8 k-iterations
+])
+def test_declared_grid_bitwise_every_policy(grid, m, n, k, tile):
+    """KernelTile.grid: a launch on g = grid workgroups (default_g honours the tile) runs the
+    reference's schedule for HardwareModel(grid, 1) item for item and stays bit-exact."""
+    sk = _sk()
+    a, b = _int_case(m, n, k, seed=m ^ n ^ k ^ grid)
+    want = ogemm.reference_gemm(a, b)
+    t = sk.kernel_tile(*tile, 0, grid)
+    for pol in (sk.Policy.data_parallel(), sk.Policy.hybrid(1), sk.Policy.all_stream_k()):
+        got, plan = _run(a, b, pol, t, trace_cap=64)
+        assert plan.g == grid
+        assert np.array_equal(got.double().cpu().numpy(), want), (grid, pol.label)
+        _assert_trace(plan, m, n, k, tile, pol)
+
+
 @pytest.mark.parametrize("out", ["fp32", "bf16"])
 @pytest.mark.parametrize("m,n,k,tile,pol", [
     (2048, 2560, 1096, (128, 128, 64), ("hybrid", 2, True)),      # multi-wave, two-contributor split tiles
