@@ -60,6 +60,7 @@ def main() -> None:
     ap.add_argument("--md", default=None)
     ap.add_argument("--tokens", default=",".join(str(1 << e) for e in range(14)))
     ap.add_argument("--oracle", action="store_true", help="time every (tile, policy) in-run (cold)")
+    ap.add_argument("--bank", default=None, help="tile bank directory (default: the shipped bank)")
     args = ap.parse_args()
 
     import torch
@@ -68,7 +69,7 @@ def main() -> None:
     from paper_2408_11417_b200 import tiles as tl
 
     out_dt = torch.bfloat16 if args.out == "bf16" else torch.float32
-    bank = tl.TileBank.load(sk.default_bank_dir())
+    bank = tl.TileBank.load(args.bank or sk.default_bank_dir())
     rows = []
     for n in (4096, 14336):
         for m in (int(v) for v in args.tokens.split(",")):
