@@ -286,7 +286,8 @@ class GemmPlan:
         one stream could otherwise be replayed concurrently on different streams and race
         on one flags/partials area.  Without this call, the first captured launch allocates
         the private workspace inside the capture (its header memset then becomes a graph
-        node).  One workspace must never serve two executions at once: a graph (like any
+        node, re-run before the GEMM on every replay); calling this first is the recommended
+        path, since it also settles the zero-fill before any launch (see ``_new_workspace``).  One workspace must never serve two executions at once: a graph (like any
         launch of this plan) must not be replayed concurrently with itself.
         """
         if self.ws_bytes and self._private_ws is None:
